@@ -118,18 +118,22 @@ def window_mask(ext: tuple, center: tuple, n: int) -> np.ndarray:
 # ---------------------------------------------------------------------------------
 # Multislice forward model G (reading #1) and loss f_i (Eq. 1; Eq. 2)
 # ---------------------------------------------------------------------------------
-def forward(probe: np.ndarray, vwin: np.ndarray, sigma: float, c: float):
+def forward(probe: np.ndarray, vwin: np.ndarray, sigma: float, c: float, dtype=np.float64):
     """psi_0 = p;  phi_s = exp(i sigma V_s) psi_s;  psi_{s+1} = F^-1(H F phi_s);  Psi = F psi_S.
 
     Returns (psi_S, Psi, [phi_0 .. phi_{S-1}]).  The propagation after the last slice
-    is applied literally (reading #5).
+    is applied literally (reading #5).  dtype=np.float32 runs the same arithmetic in
+    single precision (only to measure the fp32 floor); the oracle is float64.
     """
     n = probe.shape[0]
-    h = propagator(n, c)
-    psi = probe.astype(np.complex128)
+    cdt = np.complex64 if dtype == np.float32 else np.complex128
+    h = propagator(n, c).astype(cdt)
+    psi = probe.astype(cdt)
+    vwin = vwin.astype(dtype)
+    sigma = dtype(sigma)
     phis = []
     for s in range(vwin.shape[0]):
-        phi = np.exp(1j * sigma * vwin[s]) * psi
+        phi = np.exp(1j * sigma * vwin[s]).astype(cdt) * psi
         phis.append(phi)
         psi = ifft2(h * fft2(phi))
     return psi, fft2(psi), phis
@@ -141,7 +145,7 @@ def probe_loss(probe, vwin, amp, sigma, c) -> float:
     return float(np.sum((np.abs(big_psi) - amp) ** 2))
 
 
-def probe_grad(probe, vwin, amp, sigma, c, tau: float = TAU):
+def probe_grad(probe, vwin, amp, sigma, c, tau: float = TAU, dtype=np.float64):
     """Individual image gradient d f_i / d V over the full window (Alg. 1 step 6; Eq. 2).
 
     Adjoint of the forward chain (Wirtinger chi = d f / d conj z):
@@ -151,24 +155,26 @@ def probe_grad(probe, vwin, amp, sigma, c, tau: float = TAU):
           chi   = F^-1 (conj(H) F chi)          (chi_{phi_s})
           g_s   = 2 sigma Im(chi conj(phi_s))
           chi   = conj(exp(i sigma V_s)) chi    (chi_{psi_s})
-    Returns (g [S][N][N] float64, f_i).
+    Returns (g [S][N][N], f_i).  dtype as in forward().
     """
     n = probe.shape[0]
-    h = propagator(n, c)
-    _, big_psi, phis = forward(probe, vwin, sigma, c)
+    cdt = np.complex64 if dtype == np.float32 else np.complex128
+    h = propagator(n, c).astype(cdt)
+    vwin = vwin.astype(dtype)
+    _, big_psi, phis = forward(probe, vwin, sigma, c, dtype)
     mag = np.abs(big_psi)
-    resid = mag - amp
+    resid = mag - amp.astype(dtype)
     f = float(np.sum(resid ** 2))
     thr = tau * math.sqrt(float(np.sum(np.abs(probe) ** 2))) / n
     keep = mag > thr
     chi_big = np.zeros_like(big_psi)
     chi_big[keep] = resid[keep] * big_psi[keep] / mag[keep]
     chi = ifft2(chi_big)
-    g = np.zeros(vwin.shape, dtype=np.float64)
+    g = np.zeros(vwin.shape, dtype=dtype)
     for s in range(vwin.shape[0] - 1, -1, -1):
         chi = ifft2(np.conj(h) * fft2(chi))
         g[s] = 2.0 * sigma * np.imag(chi * np.conj(phis[s]))
-        chi = np.conj(np.exp(1j * sigma * vwin[s])) * chi
+        chi = np.conj(np.exp(1j * dtype(sigma) * vwin[s])).astype(cdt) * chi
     return g, f
 
 

@@ -1,0 +1,1019 @@
+// Host side of the C ABI (include/ptycho.h): geometry, workspace carving, per-probe pass
+// schedule (CUDA graph per tile), APPP hop schedule (device copies / NCCL P2P), stitch.
+//
+// Paper anchors: Alg. 1, §Image Gradient Decomposition, §Forward and
+// Backward Accumulated Gradients Pass, APPP.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "ptycho.h"
+
+using namespace ptycho;
+
+namespace {
+
+struct Hop {       // one APPP message: dst (op)= src on region [y0,y1) x [x0,x1), all slices
+  int src, dst;
+  int y0, y1, x0, x1;
+  int add;         // 1 = ADD (forward passes), 0 = REPLACE (backward passes)
+};
+
+struct Tile {
+  int k = 0, r = 0, c = 0, owner = 0;
+  int iy0 = 0, ix0 = 0, iy1 = 0, ix1 = 0;  // interior
+  int ey0 = 0, ex0 = 0, ey1 = 0, ex1 = 0;  // extended rect R_k
+  int eh = 0, ew = 0;
+  int pitch0 = 0, pitch1 = 0;
+  long long slice_stride = 0;
+  std::vector<int64_t> probes;  // global ids, ascending
+  // device state (local tiles only)
+  float* V = nullptr;
+  float* acc = nullptr;
+  float2* stash = nullptr;
+  float2* wf[2] = {nullptr, nullptr};
+  float* amp = nullptr;
+  int2* centers = nullptr;
+  int* cursor = nullptr;
+  unsigned* done = nullptr;
+  double* loss_part = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev = nullptr;
+  cudaGraphExec_t graph = nullptr;
+};
+
+constexpr size_t ALIGN = 256;
+size_t align_up(size_t x, size_t a = ALIGN) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct ptycho_ctx_s {
+  ptycho_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // tiles
+  bool tiles_set = false;
+  int R = 0, C = 0, halo = 0, rank = 0, nranks = 1;
+  std::vector<Tile> tiles;
+  std::vector<int> local;  // local tile indices, increasing
+  std::vector<Hop> hops;
+  ncclComm_t comm = nullptr;
+  // scan
+  bool scan_set = false;
+  std::vector<int32_t> centers;
+  // workspace
+  bool ws_set = false;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  float2* wtab = nullptr;
+  float2* htab = nullptr;
+  float2* probe = nullptr;
+  double* dscratch = nullptr;
+  int* iscratch = nullptr;
+  float* staging = nullptr;
+  size_t staging_floats = 0;
+  float* debug = nullptr;
+  size_t debug_floats = 0;
+  float* sendbuf = nullptr;
+  float* recvbuf = nullptr;
+  size_t msg_floats = 0;
+  bool probe_set = false;
+  double probe_norm = 1.0;
+  std::vector<float2> h_wtab, h_htab;
+  long long launches = 0;
+  cudaEvent_t ev_fork = nullptr;
+  bool use_graph = true;
+  bool use_pdl = true;
+};
+
+static thread_local std::string g_create_err;
+
+static ptycho_status fail(ptycho_ctx ctx, ptycho_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  else g_create_err = buf;
+  return st;
+}
+
+#define CK(expr)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess) return fail(ctx, PTYCHO_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define NK(expr)                                                                                  \
+  do {                                                                                            \
+    ncclResult_t r_ = (expr);                                                                     \
+    if (r_ != ncclSuccess) return fail(ctx, PTYCHO_ENCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+#define PASS(expr)                                                                                \
+  do {                                                                                            \
+    ptycho_status s_ = (expr);                                                                    \
+    if (s_ != PTYCHO_OK) return s_;                                                               \
+  } while (0)
+
+static int slices_even(int S) { return (S + 1) / 2; }
+static int slices_odd(int S) { return S / 2; }
+
+// ------------------------------------------------------------------------------------------
+// tiny device helpers launched from here
+// ------------------------------------------------------------------------------------------
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+// ------------------------------------------------------------------------------------------
+// lifecycle
+// ------------------------------------------------------------------------------------------
+extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, void* cuda_stream, ptycho_ctx* out) {
+  ptycho_ctx ctx = nullptr;
+  if (!cfg || !out) return fail(ctx, PTYCHO_EARG, "cfg and out must be non-NULL");
+  if (cfg->n != 64 && cfg->n != 256 && cfg->n != 1024)
+    return fail(ctx, PTYCHO_EARG, "n = %d: supported windows are 64, 256, 1024", cfg->n);
+  if (cfg->slices < 1 || cfg->height < 1 || cfg->width < 1)
+    return fail(ctx, PTYCHO_EARG, "slices/height/width must be >= 1");
+  if (cfg->pass_period < 0) return fail(ctx, PTYCHO_EARG, "pass_period T must be >= 0");
+  if (!(cfg->tau >= 0.f)) return fail(ctx, PTYCHO_EARG, "tau must be >= 0");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(ctx, PTYCHO_ECUDA, "CUDA device %d not available", device);
+  ctx = new ptycho_ctx_s();
+  ctx->cfg = *cfg;
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  if (const char* e = getenv("PTYCHO_NO_GRAPH")) ctx->use_graph = atoi(e) == 0;
+  if (const char* e = getenv("PTYCHO_NO_PDL")) ctx->use_pdl = atoi(e) == 0;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    fail(nullptr, PTYCHO_ECUDA, "cuda init: %s", cudaGetErrorString(e));
+    delete ctx;
+    return PTYCHO_ECUDA;
+  }
+  // tables in double, rounded to float: W_N^k and H_1[u]/N (reading #3, #4)
+  const int n = cfg->n;
+  ctx->h_wtab.resize(n);
+  ctx->h_htab.resize(n);
+  for (int k = 0; k < n; ++k) {
+    const double th = -2.0 * M_PI * (double)k / (double)n;
+    ctx->h_wtab[k] = make_float2((float)std::cos(th), (float)std::sin(th));
+    const double m = (k < n / 2) ? (double)k : (double)(k - n);
+    const double ph = -M_PI * (double)cfg->prop_c * m * m / ((double)n * (double)n);
+    ctx->h_htab[k] = make_float2((float)(std::cos(ph) / n), (float)(std::sin(ph) / n));
+  }
+  *out = ctx;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_destroy(ptycho_ctx ctx) {
+  if (!ctx) return PTYCHO_OK;
+  cudaSetDevice(ctx->device);
+  for (auto& t : ctx->tiles) {
+    if (t.graph) cudaGraphExecDestroy(t.graph);
+    if (t.stream) cudaStreamDestroy(t.stream);
+    if (t.ev) cudaEventDestroy(t.ev);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  delete ctx;
+  return PTYCHO_OK;
+}
+
+extern "C" const char* ptycho_last_error(ptycho_ctx ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+extern "C" ptycho_status ptycho_nccl_unique_id(void* out, size_t bytes) {
+  ptycho_ctx ctx = nullptr;
+  if (!out || bytes < sizeof(ncclUniqueId)) return fail(ctx, PTYCHO_EARG, "need %zu bytes", sizeof(ncclUniqueId));
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return PTYCHO_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// geometry (readings #13-#16, #21)
+// ------------------------------------------------------------------------------------------
+static void split(int extent, int parts, int p, int* a, int* b) {
+  const int base = extent / parts;
+  *a = p * base;
+  *b = (p == parts - 1) ? extent : (p + 1) * base;
+}
+
+extern "C" ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t cols, int32_t halo,
+                                          const int32_t* tile_owner, const void* nccl_id, int32_t rank,
+                                          int32_t nranks) {
+  if (!ctx) return PTYCHO_EARG;
+  if (ctx->tiles_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles already called");
+  const auto& cfg = ctx->cfg;
+  if (rows < 1 || cols < 1 || rows > cfg.height || cols > cfg.width || halo < 0)
+    return fail(ctx, PTYCHO_EARG, "bad grid %dx%d halo %d for object %dx%d", rows, cols, halo, cfg.height, cfg.width);
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, PTYCHO_EARG, "bad rank %d / %d", rank, nranks);
+  if (nranks > 1 && !nccl_id) return fail(ctx, PTYCHO_EARG, "nccl_id required when nranks > 1");
+  ctx->R = rows;
+  ctx->C = cols;
+  ctx->halo = halo;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  ctx->tiles.assign(rows * cols, Tile());
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) {
+      Tile& t = ctx->tiles[r * cols + c];
+      t.k = r * cols + c;
+      t.r = r;
+      t.c = c;
+      split(cfg.height, rows, r, &t.iy0, &t.iy1);
+      split(cfg.width, cols, c, &t.ix0, &t.ix1);
+      t.ey0 = std::max(0, t.iy0 - halo);
+      t.ex0 = std::max(0, t.ix0 - halo);
+      t.ey1 = std::min(cfg.height, t.iy1 + halo);
+      t.ex1 = std::min(cfg.width, t.ix1 + halo);
+      t.eh = t.ey1 - t.ey0;
+      t.ew = t.ex1 - t.ex0;
+      t.pitch0 = (t.ew + 31) / 32 * 32;
+      t.pitch1 = (t.eh + 31) / 32 * 32;
+      const long long a = (long long)t.eh * t.pitch0, b = (long long)t.ew * t.pitch1;
+      t.slice_stride = (std::max(a, b) + 31) / 32 * 32;
+      t.owner = tile_owner ? tile_owner[t.k] : rank;
+      if (t.owner < 0 || t.owner >= nranks) return fail(ctx, PTYCHO_EARG, "tile_owner[%d] = %d", t.k, t.owner);
+      if (t.owner == rank) ctx->local.push_back(t.k);
+    }
+  // APPP hop list in the global order every rank follows (Fig. forward_backward a-d)
+  auto T = [&](int r, int c) -> Tile& { return ctx->tiles[r * cols + c]; };
+  for (int c = 0; c < cols; ++c)
+    for (int r = 0; r + 1 < rows; ++r) {  // vertical forward: ADD down the column
+      Tile &a = T(r, c), &b = T(r + 1, c);
+      ctx->hops.push_back({a.k, b.k, std::max(a.ey0, b.ey0), std::min(a.ey1, b.ey1), a.ex0, a.ex1, 1});
+    }
+  for (int c = 0; c < cols; ++c)
+    for (int r = rows - 1; r >= 1; --r) {  // vertical backward: REPLACE up the column
+      Tile &a = T(r, c), &b = T(r - 1, c);
+      ctx->hops.push_back({a.k, b.k, std::max(a.ey0, b.ey0), std::min(a.ey1, b.ey1), a.ex0, a.ex1, 0});
+    }
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c + 1 < cols; ++c) {  // horizontal forward over the full extended height Y_r
+      Tile &a = T(r, c), &b = T(r, c + 1);
+      ctx->hops.push_back({a.k, b.k, a.ey0, a.ey1, std::max(a.ex0, b.ex0), std::min(a.ex1, b.ex1), 1});
+    }
+  for (int r = 0; r < rows; ++r)
+    for (int c = cols - 1; c >= 1; --c) {  // horizontal backward
+      Tile &a = T(r, c), &b = T(r, c - 1);
+      ctx->hops.push_back({a.k, b.k, a.ey0, a.ey1, std::max(a.ex0, b.ex0), std::min(a.ex1, b.ex1), 0});
+    }
+  CK(cudaSetDevice(ctx->device));
+  for (int k : ctx->local) {
+    CK(cudaStreamCreateWithFlags(&ctx->tiles[k].stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->tiles[k].ev, cudaEventDisableTiming));
+  }
+  if (nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    NK(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+  }
+  ctx->tiles_set = true;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_set_scan(ptycho_ctx ctx, const int32_t* centers_yx, int64_t n_probes) {
+  if (!ctx) return PTYCHO_EARG;
+  if (!ctx->tiles_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles must precede set_scan");
+  if (ctx->scan_set) return fail(ctx, PTYCHO_ESTATE, "set_scan already called");
+  if (n_probes < 0 || (n_probes > 0 && !centers_yx)) return fail(ctx, PTYCHO_EARG, "bad scan");
+  const auto& cfg = ctx->cfg;
+  const int n = cfg.n;
+  ctx->centers.assign(centers_yx, centers_yx + 2 * n_probes);
+  for (int64_t i = 0; i < n_probes; ++i) {
+    const int cy = centers_yx[2 * i], cx = centers_yx[2 * i + 1];
+    if (cy < 0 || cy >= cfg.height || cx < 0 || cx >= cfg.width)
+      return fail(ctx, PTYCHO_EARG, "probe %lld centre (%d,%d) outside the %dx%d object", (long long)i, cy, cx,
+                  cfg.height, cfg.width);
+    // centre containment in half-open interiors (reading #15): row/column by the uniform split
+    const int base_y = cfg.height / ctx->R, base_x = cfg.width / ctx->C;
+    const int r = std::min(cy / base_y, ctx->R - 1), c = std::min(cx / base_x, ctx->C - 1);
+    Tile& t = ctx->tiles[r * ctx->C + c];
+    if (cfg.flags & PTYCHO_F_EXACT_WINDOW) {
+      const int wy0 = std::max(cy - n / 2, 0), wy1 = std::min(cy - n / 2 + n, cfg.height);
+      const int wx0 = std::max(cx - n / 2, 0), wx1 = std::min(cx - n / 2 + n, cfg.width);
+      if (wy0 < t.ey0 || wy1 > t.ey1 || wx0 < t.ex0 || wx1 > t.ex1)
+        return fail(ctx, PTYCHO_EHALO, "probe %lld window not covered by tile %d's extended rect (halo %d < %d)",
+                    (long long)i, t.k, ctx->halo, n / 2);
+    }
+    t.probes.push_back(i);
+  }
+  ctx->scan_set = true;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_local_probes(ptycho_ctx ctx, int64_t* ids, int64_t* count) {
+  if (!ctx || !count) return PTYCHO_EARG;
+  if (!ctx->scan_set) return fail(ctx, PTYCHO_ESTATE, "set_scan first");
+  int64_t m = 0;
+  for (int k : ctx->local)
+    for (int64_t g : ctx->tiles[k].probes) {
+      if (ids) ids[m] = g;
+      ++m;
+    }
+  *count = m;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_tile_probe_count(ptycho_ctx ctx, int32_t tile, int64_t* count) {
+  if (!ctx || !count) return PTYCHO_EARG;
+  if (!ctx->scan_set) return fail(ctx, PTYCHO_ESTATE, "set_scan first");
+  if (tile < 0 || tile >= (int)ctx->tiles.size()) return fail(ctx, PTYCHO_EARG, "bad tile %d", tile);
+  *count = (int64_t)ctx->tiles[tile].probes.size();
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_tile_rect(ptycho_ctx ctx, int32_t tile, int32_t ext[4], int32_t interior[4]) {
+  if (!ctx) return PTYCHO_EARG;
+  if (!ctx->tiles_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles first");
+  if (tile < 0 || tile >= (int)ctx->tiles.size()) return fail(ctx, PTYCHO_EARG, "bad tile %d", tile);
+  const Tile& t = ctx->tiles[tile];
+  if (ext) {
+    ext[0] = t.ey0; ext[1] = t.ex0; ext[2] = t.ey1; ext[3] = t.ex1;
+  }
+  if (interior) {
+    interior[0] = t.iy0; interior[1] = t.ix0; interior[2] = t.iy1; interior[3] = t.ix1;
+  }
+  return PTYCHO_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// workspace
+// ------------------------------------------------------------------------------------------
+static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
+  const auto& cfg = ctx->cfg;
+  const size_t n = cfg.n, n2 = n * n, S = cfg.slices;
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    char* p = carve ? ctx->ws + off : nullptr;
+    off = align_up(off + bytes);
+    return p;
+  };
+  ctx->wtab = (float2*)take(n * sizeof(float2));
+  ctx->htab = (float2*)take(n * sizeof(float2));
+  ctx->probe = (float2*)take(n2 * sizeof(float2));
+  ctx->dscratch = (double*)take(64 * sizeof(double));
+  ctx->iscratch = (int*)take(64 * sizeof(int));
+  ctx->staging_floats = std::max<size_t>((size_t)cfg.height * cfg.width, 8 * n2);
+  ctx->staging = (float*)take(ctx->staging_floats * sizeof(float));
+  ctx->debug_floats = std::max<size_t>(S, 2) * n2;
+  ctx->debug = (float*)take(ctx->debug_floats * sizeof(float));
+  if (ctx->nranks > 1) {
+    size_t mx = 0;
+    for (const Hop& h : ctx->hops) {
+      const size_t area = (size_t)std::max(0, h.y1 - h.y0) * std::max(0, h.x1 - h.x0);
+      mx = std::max(mx, area);
+    }
+    for (const Tile& t : ctx->tiles) mx = std::max(mx, (size_t)(t.iy1 - t.iy0) * (t.ix1 - t.ix0));
+    // messages are slabs of whole slices, at least one slice, at most ~64 MB
+    ctx->msg_floats = std::max(mx, (size_t)(16u << 20));
+    ctx->sendbuf = (float*)take(ctx->msg_floats * sizeof(float));
+    ctx->recvbuf = (float*)take(ctx->msg_floats * sizeof(float));
+  }
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const size_t vol = (size_t)t.slice_stride * S;
+    t.V = (float*)take(vol * sizeof(float));
+    t.acc = (float*)take(vol * sizeof(float));
+    t.stash = (float2*)take(S * n2 * sizeof(float2));
+    t.wf[0] = (float2*)take(n2 * sizeof(float2));
+    t.wf[1] = (float2*)take(n2 * sizeof(float2));
+    t.amp = (float*)take(std::max<size_t>(t.probes.size(), 1) * n2 * sizeof(float));
+    t.centers = (int2*)take(std::max<size_t>(t.probes.size(), 1) * sizeof(int2));
+    t.cursor = (int*)take(sizeof(int));
+    t.done = (unsigned*)take(sizeof(unsigned));
+    t.loss_part = (double*)take((n / LINES_PER_CTA) * sizeof(double));
+  }
+  return off;
+}
+
+extern "C" ptycho_status ptycho_workspace_bytes(ptycho_ctx ctx, size_t* bytes) {
+  if (!ctx || !bytes) return PTYCHO_EARG;
+  if (!ctx->tiles_set || !ctx->scan_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles and set_scan first");
+  *bytes = plan_workspace(ctx, false);
+  return PTYCHO_OK;
+}
+
+static ptycho_status zero_tiles(ptycho_ctx ctx, bool v, bool a) {
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const size_t vol = (size_t)t.slice_stride * ctx->cfg.slices;
+    if (v) CK(cudaMemsetAsync(t.V, 0, vol * sizeof(float), ctx->stream));
+    if (a) CK(cudaMemsetAsync(t.acc, 0, vol * sizeof(float), ctx->stream));
+  }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_dev, size_t bytes) {
+  if (!ctx) return PTYCHO_EARG;
+  if (!ctx->tiles_set || !ctx->scan_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles and set_scan first");
+  if (ctx->ws_set) return fail(ctx, PTYCHO_ESTATE, "set_workspace already called");
+  if (!workspace_dev || ((uintptr_t)workspace_dev % ALIGN)) return fail(ctx, PTYCHO_EARG, "workspace must be 256-B aligned");
+  const size_t need = plan_workspace(ctx, false);
+  if (bytes < need) return fail(ctx, PTYCHO_ENOMEM, "workspace %zu B < required %zu B", bytes, need);
+  CK(cudaSetDevice(ctx->device));
+  ctx->ws = (char*)workspace_dev;
+  ctx->ws_bytes = bytes;
+  plan_workspace(ctx, true);
+  const size_t n = ctx->cfg.n;
+  CK(cudaMemcpyAsync(ctx->wtab, ctx->h_wtab.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->htab, ctx->h_htab.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    std::vector<int2> hc(std::max<size_t>(t.probes.size(), 1), make_int2(0, 0));
+    for (size_t j = 0; j < t.probes.size(); ++j)
+      hc[j] = make_int2(ctx->centers[2 * t.probes[j]], ctx->centers[2 * t.probes[j] + 1]);
+    CK(cudaMemcpyAsync(t.centers, hc.data(), hc.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(t.cursor, 0, sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(t.done, 0, sizeof(unsigned), ctx->stream));
+    CK(cudaMemsetAsync(t.loss_part, 0, (n / LINES_PER_CTA) * sizeof(double), ctx->stream));
+    CK(cudaMemsetAsync(t.amp, 0, std::max<size_t>(t.probes.size(), 1) * n * n * sizeof(float), ctx->stream));
+  }
+  PASS(zero_tiles(ctx, true, true));
+  CK(cudaStreamSynchronize(ctx->stream));  // host vectors above go out of scope
+  ctx->ws_set = true;
+  return PTYCHO_OK;
+}
+
+static ptycho_status need_ws(ptycho_ctx ctx) {
+  if (!ctx) return PTYCHO_EARG;
+  if (!ctx->ws_set) return fail(ctx, PTYCHO_ESTATE, "set_workspace first");
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_set_probe(ptycho_ctx ctx, const void* probe_c64, int on_device) {
+  PASS(need_ws(ctx));
+  if (!probe_c64) return fail(ctx, PTYCHO_EARG, "probe is NULL");
+  const size_t n2 = (size_t)ctx->cfg.n * ctx->cfg.n;
+  CK(cudaSetDevice(ctx->device));
+  std::vector<float2> h(n2);
+  if (on_device) CK(cudaMemcpy(h.data(), probe_c64, n2 * sizeof(float2), cudaMemcpyDeviceToHost));
+  else memcpy(h.data(), probe_c64, n2 * sizeof(float2));
+  double nrm = 0.0;
+  for (auto& v : h) nrm += (double)v.x * v.x + (double)v.y * v.y;
+  ctx->probe_norm = std::sqrt(nrm);
+  CK(cudaMemcpyAsync(ctx->probe, h.data(), n2 * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->probe_set = true;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_load_measurements(ptycho_ctx ctx, const float* amp, int on_device,
+                                                  int64_t first_local, int64_t count, int32_t layout_flags) {
+  PASS(need_ws(ctx));
+  int64_t nloc = 0;
+  for (int k : ctx->local) nloc += (int64_t)ctx->tiles[k].probes.size();
+  if (count < 0 || first_local < 0 || first_local + count > nloc)
+    return fail(ctx, PTYCHO_EARG, "range [%lld, %lld) outside the %lld local probes", (long long)first_local,
+                (long long)(first_local + count), (long long)nloc);
+  if (count == 0) return PTYCHO_OK;
+  if (!amp) return fail(ctx, PTYCHO_EARG, "amp is NULL");
+  CK(cudaSetDevice(ctx->device));
+  const int n = ctx->cfg.n;
+  const size_t n2 = (size_t)n * n;
+  const int shift = (layout_flags & PTYCHO_AMP_DC_CENTERED) ? 1 : 0;
+  const int inten = (layout_flags & PTYCHO_AMP_INTENSITY) ? 1 : 0;
+  const int transpose = ctx->cfg.slices & 1;  // store in the turnaround pass's layout L_{S&1}
+  const int64_t chunk = (int64_t)(ctx->staging_floats / n2);
+  int64_t g = 0;  // local index of the first probe of the current tile
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const int64_t nk = (int64_t)t.probes.size();
+    const int64_t lo = std::max(first_local, g), hi = std::min(first_local + count, g + nk);
+    for (int64_t p = lo; p < hi;) {
+      const int64_t m = on_device ? (hi - p) : std::min(chunk, hi - p);
+      const float* src = amp + (size_t)(p - first_local) * n2;
+      if (!on_device) {
+        CK(cudaMemcpyAsync(ctx->staging, src, (size_t)m * n2 * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        src = ctx->staging;
+      }
+      CK(launch_amp_load(t.amp + (size_t)(p - g) * n2, src, (int)m, n, shift, inten, transpose, ctx->stream));
+      ++ctx->launches;
+      p += m;
+    }
+    g += nk;
+  }
+  if (!on_device) CK(cudaStreamSynchronize(ctx->stream));
+  return PTYCHO_OK;
+}
+
+// slice pointers / region helpers for the alternating per-slice layout
+struct SliceView {
+  float* base;       // first element of the region in the first slice of this parity
+  long long ld;      // row pitch
+  long long ss;      // stride between slices of this parity (2 * slice_stride)
+  int rows, cols, nslices;
+};
+
+static SliceView region_view(const Tile& t, float* buf, int parity, int S, int y0, int y1, int x0, int x1) {
+  SliceView v;
+  v.ss = 2 * t.slice_stride;
+  v.nslices = parity ? slices_odd(S) : slices_even(S);
+  if (parity == 0) {
+    v.base = buf + (long long)(y0 - t.ey0) * t.pitch0 + (x0 - t.ex0);
+    v.ld = t.pitch0;
+    v.rows = y1 - y0;
+    v.cols = x1 - x0;
+  } else {
+    v.base = buf + t.slice_stride + (long long)(x0 - t.ex0) * t.pitch1 + (y0 - t.ey0);
+    v.ld = t.pitch1;
+    v.rows = x1 - x0;
+    v.cols = y1 - y0;
+  }
+  return v;
+}
+
+// global slice [H][W] (row pitch W) <-> tile slice s on the rect [y0,y1)x[x0,x1)
+static ptycho_status global_to_tile(ptycho_ctx ctx, const Tile& t, float* buf, int s, const float* g, int y0, int y1,
+                                    int x0, int x1) {
+  const int W = ctx->cfg.width;
+  float* sl = buf + (long long)s * t.slice_stride;
+  const float* gp = g + (long long)y0 * W + x0;
+  if ((s & 1) == 0) {
+    CK(launch_copy2d(sl + (long long)(y0 - t.ey0) * t.pitch0 + (x0 - t.ex0), t.pitch0, 0, gp, W, 0, y1 - y0, x1 - x0,
+                     1, 0, ctx->stream));
+  } else {  // tile[x][y] = g[y][x]
+    CK(launch_transpose2d(sl + (long long)(x0 - t.ex0) * t.pitch1 + (y0 - t.ey0), t.pitch1, 0, gp, W, 0, x1 - x0,
+                          y1 - y0, 1, 0, ctx->stream));
+  }
+  ++ctx->launches;
+  return PTYCHO_OK;
+}
+
+static ptycho_status tile_to_global(ptycho_ctx ctx, const Tile& t, const float* buf, int s, float* g, int y0, int y1,
+                                    int x0, int x1) {
+  const int W = ctx->cfg.width;
+  const float* sl = buf + (long long)s * t.slice_stride;
+  float* gp = g + (long long)y0 * W + x0;
+  if ((s & 1) == 0) {
+    CK(launch_copy2d(gp, W, 0, sl + (long long)(y0 - t.ey0) * t.pitch0 + (x0 - t.ex0), t.pitch0, 0, y1 - y0, x1 - x0,
+                     1, 0, ctx->stream));
+  } else {  // g[y][x] = tile[x][y]
+    CK(launch_transpose2d(gp, W, 0, sl + (long long)(x0 - t.ex0) * t.pitch1 + (y0 - t.ey0), t.pitch1, 0, y1 - y0,
+                          x1 - x0, 1, 0, ctx->stream));
+  }
+  ++ctx->launches;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_set_volume(ptycho_ctx ctx, const float* volume, int on_device) {
+  PASS(need_ws(ctx));
+  CK(cudaSetDevice(ctx->device));
+  const auto& cfg = ctx->cfg;
+  PASS(zero_tiles(ctx, true, true));
+  if (!volume) return PTYCHO_OK;  // V_0 = 0
+  const size_t hw = (size_t)cfg.height * cfg.width;
+  for (int s = 0; s < cfg.slices; ++s) {
+    const float* g = volume + (size_t)s * hw;
+    if (!on_device) {
+      CK(cudaMemcpyAsync(ctx->staging, g, hw * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+      g = ctx->staging;
+    }
+    for (int k : ctx->local) {
+      const Tile& t = ctx->tiles[k];
+      PASS(global_to_tile(ctx, t, t.V, s, g, t.ey0, t.ey1, t.ex0, t.ex1));
+    }
+    if (!on_device) CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return PTYCHO_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// the per-probe pass chain (DESIGN.md §Pass schedule): 2S+1 kernels
+// ------------------------------------------------------------------------------------------
+enum ChainMode { CHAIN_GRAD = 0, CHAIN_SIMULATE, CHAIN_DEBUG_GRAD, CHAIN_DEBUG_EXIT };
+
+static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
+  PassArgs a{};
+  a.V = t.V;
+  a.acc = t.acc;
+  a.slice_stride = t.slice_stride;
+  a.pitch0 = t.pitch0;
+  a.pitch1 = t.pitch1;
+  a.ey0 = t.ey0;
+  a.ex0 = t.ex0;
+  a.eh = t.eh;
+  a.ew = t.ew;
+  a.stash = t.stash;
+  a.probe = ctx->probe;
+  a.amp = t.amp;
+  a.centers = t.centers;
+  a.cursor = t.cursor;
+  a.done = t.done;
+  a.loss_part = t.loss_part;
+  a.wtab = ctx->wtab;
+  a.htab = ctx->htab;
+  a.sigma = ctx->cfg.sigma;
+  a.alpha = ctx->cfg.alpha;
+  a.thr = (float)(ctx->cfg.tau * ctx->probe_norm / ctx->cfg.n);
+  return a;
+}
+
+static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cudaStream_t st) {
+  const int S = ctx->cfg.slices, n = ctx->cfg.n;
+  PassArgs a = base_args(ctx, t);
+  int pass = 0;
+  auto go = [&](PassKind kind, int s, bool last) -> ptycho_status {
+    PassArgs b = a;
+    b.s = s;
+    b.in = t.wf[pass & 1];
+    b.out = t.wf[(pass + 1) & 1];
+    b.advance = (last && (mode == CHAIN_GRAD || mode == CHAIN_SIMULATE)) ? 1 : 0;
+    if (mode == CHAIN_DEBUG_GRAD) b.gexport = ctx->debug;
+    if (mode == CHAIN_DEBUG_EXIT) {
+      b.natural_out = (float2*)ctx->debug;
+      b.natural_transposed = S & 1;
+    }
+    CK(launch_pass(n, kind, b, st, ctx->use_pdl));
+    ++ctx->launches;
+    ++pass;
+    return PTYCHO_OK;
+  };
+  // forward: pass s finishes psi_s's propagation along its axis, transmits, starts the next
+  const bool exit_mode = (mode == CHAIN_DEBUG_EXIT);
+  if (S == 1) {
+    PASS(go(exit_mode ? K_FWD_FIRST_PROP : K_FWD_FIRST_FFT, 0, false));
+  } else {
+    PASS(go(K_FWD_FIRST_PROP, 0, false));
+    for (int s = 1; s < S - 1; ++s) PASS(go(K_FWD_MID, s, false));
+    PASS(go(exit_mode ? K_FWD_MID : K_FWD_LAST, S - 1, false));
+  }
+  if (exit_mode) return go(K_EXIT_COMPLETE, S, true);
+  if (mode == CHAIN_SIMULATE) return go(K_SIMULATE, S, true);
+  PASS(go(K_TURN, S, false));
+  if (S == 1) return go(K_BWD_LAST_END, 0, true);
+  PASS(go(K_BWD_LAST_PROP, S - 1, false));
+  for (int s = S - 2; s >= 1; --s) PASS(go(K_BWD_MID, s, false));
+  return go(K_BWD_END, 0, true);
+}
+
+static int chain_len(int S) { return 2 * S + 1; }
+
+static ptycho_status ensure_graph(ptycho_ctx ctx, Tile& t) {
+  if (t.graph || !ctx->use_graph) return PTYCHO_OK;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(t.stream, cudaStreamCaptureModeThreadLocal));
+  const long long before = ctx->launches;
+  ptycho_status st = enqueue_chain(ctx, t, CHAIN_GRAD, t.stream);
+  cudaError_t e = cudaStreamEndCapture(t.stream, &g);
+  ctx->launches = before;  // captured, not launched
+  if (st != PTYCHO_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  CK(e);
+  e = cudaGraphInstantiateWithFlags(&t.graph, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  return PTYCHO_OK;
+}
+
+static ptycho_status set_cursor(ptycho_ctx ctx, Tile& t, int v, cudaStream_t st) {
+  set_int_kernel<<<1, 1, 0, st>>>(t.cursor, v);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return PTYCHO_OK;
+}
+
+static ptycho_status fork_tiles(ptycho_ctx ctx) {
+  CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  for (int k : ctx->local) CK(cudaStreamWaitEvent(ctx->tiles[k].stream, ctx->ev_fork, 0));
+  return PTYCHO_OK;
+}
+
+static ptycho_status join_tiles(ptycho_ctx ctx) {
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    CK(cudaEventRecord(t.ev, t.stream));
+    CK(cudaStreamWaitEvent(ctx->stream, t.ev, 0));
+  }
+  return PTYCHO_OK;
+}
+
+static ptycho_status need_run(ptycho_ctx ctx) {
+  PASS(need_ws(ctx));
+  if (!ctx->probe_set) return fail(ctx, PTYCHO_ESTATE, "set_probe first");
+  return PTYCHO_OK;
+}
+
+static ptycho_status sum_loss(ptycho_ctx ctx, double* out_host) {
+  // fixed-order sum: per tile (deterministic kernel), then tiles in increasing index on the host
+  const int parts = ctx->cfg.n / LINES_PER_CTA;
+  int j = 0;
+  for (int k : ctx->local) {
+    CK(launch_sum_double(ctx->tiles[k].loss_part, parts, ctx->dscratch + j, ctx->stream));
+    ++ctx->launches;
+    ++j;
+  }
+  std::vector<double> h(std::max(j, 1), 0.0);
+  if (j) CK(cudaMemcpyAsync(h.data(), ctx->dscratch, j * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double tot = 0.0;
+  for (int i = 0; i < j; ++i) tot += h[i];
+  *out_host = tot;
+  return PTYCHO_OK;
+}
+
+static ptycho_status zero_loss(ptycho_ctx ctx) {
+  for (int k : ctx->local)
+    CK(cudaMemsetAsync(ctx->tiles[k].loss_part, 0, (ctx->cfg.n / LINES_PER_CTA) * sizeof(double), ctx->stream));
+  return PTYCHO_OK;
+}
+
+static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, ChainMode mode) {
+  PASS(fork_tiles(ctx));
+  int64_t maxn = 0;
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const int64_t nk = (int64_t)t.probes.size();
+    const int64_t m = std::max<int64_t>(0, std::min(first + count, nk) - first);
+    maxn = std::max(maxn, m);
+    if (m > 0) PASS(set_cursor(ctx, t, (int)first, t.stream));
+    if (mode == CHAIN_GRAD) PASS(ensure_graph(ctx, t));
+  }
+  // interleave the tiles' probe chains so every tile stream is fed
+  for (int64_t j = 0; j < maxn; ++j)
+    for (int k : ctx->local) {
+      Tile& t = ctx->tiles[k];
+      const int64_t nk = (int64_t)t.probes.size();
+      if (first + j >= nk) continue;
+      if (mode == CHAIN_GRAD && t.graph) {
+        CK(cudaGraphLaunch(t.graph, t.stream));
+        ctx->launches += chain_len(ctx->cfg.slices);
+      } else {
+        PASS(enqueue_chain(ctx, t, mode, t.stream));
+      }
+    }
+  return join_tiles(ctx);
+}
+
+extern "C" ptycho_status ptycho_forward_grad(ptycho_ctx ctx, int64_t first, int64_t count, double* loss_out) {
+  PASS(need_run(ctx));
+  if (first < 0 || count < 0) return fail(ctx, PTYCHO_EARG, "bad probe range");
+  CK(cudaSetDevice(ctx->device));
+  if (loss_out) PASS(zero_loss(ctx));
+  PASS(run_probes(ctx, first, count, CHAIN_GRAD));
+  if (loss_out) PASS(sum_loss(ctx, loss_out));
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_simulate_measurements(ptycho_ctx ctx) {
+  PASS(need_run(ctx));
+  CK(cudaSetDevice(ctx->device));
+  int64_t maxn = 0;
+  for (int k : ctx->local) maxn = std::max<int64_t>(maxn, (int64_t)ctx->tiles[k].probes.size());
+  return run_probes(ctx, 0, maxn, CHAIN_SIMULATE);
+}
+
+// ------------------------------------------------------------------------------------------
+// APPP passes (Alg. 1 steps 10-13) and the accumulated step (steps 14-16)
+// ------------------------------------------------------------------------------------------
+static ptycho_status hop_local(ptycho_ctx ctx, const Hop& h) {
+  const Tile& a = ctx->tiles[h.src];
+  const Tile& b = ctx->tiles[h.dst];
+  const int S = ctx->cfg.slices;
+  for (int par = 0; par < 2; ++par) {
+    SliceView vs = region_view(a, a.acc, par, S, h.y0, h.y1, h.x0, h.x1);
+    SliceView vd = region_view(b, b.acc, par, S, h.y0, h.y1, h.x0, h.x1);
+    CK(launch_copy2d(vd.base, vd.ld, vd.ss, vs.base, vs.ld, vs.ss, vs.rows, vs.cols, vs.nslices, h.add, ctx->stream));
+    ++ctx->launches;
+  }
+  return PTYCHO_OK;
+}
+
+// Remote hop: the region is moved in slabs of whole slices, packed [slice][rows][cols] per
+// parity (even slices [y][x], odd [x][y]); sender packs + ncclSend, receiver ncclRecv + (add|copy).
+static ptycho_status hop_remote(ptycho_ctx ctx, const Hop& h, bool sender) {
+  const Tile& me = ctx->tiles[sender ? h.src : h.dst];
+  const int peer = ctx->tiles[sender ? h.dst : h.src].owner;
+  const int S = ctx->cfg.slices;
+  const size_t area = (size_t)(h.y1 - h.y0) * (h.x1 - h.x0);
+  const int slab = (int)std::max<size_t>(1, ctx->msg_floats / area);
+  for (int par = 0; par < 2; ++par) {
+    SliceView v = region_view(me, me.acc, par, S, h.y0, h.y1, h.x0, h.x1);
+    for (int z0 = 0; z0 < v.nslices; z0 += slab) {
+      const int nz = std::min(slab, v.nslices - z0);
+      const size_t cnt = area * nz;
+      float* base = v.base + (long long)z0 * v.ss;
+      const long long per = (long long)v.rows * v.cols;
+      if (sender) {
+        CK(launch_copy2d(ctx->sendbuf, v.cols, per, base, v.ld, v.ss, v.rows, v.cols, nz, 0, ctx->stream));
+        ++ctx->launches;
+        NK(ncclSend(ctx->sendbuf, cnt, ncclFloat, peer, ctx->comm, ctx->stream));
+      } else {
+        NK(ncclRecv(ctx->recvbuf, cnt, ncclFloat, peer, ctx->comm, ctx->stream));
+        CK(launch_copy2d(base, v.ld, v.ss, ctx->recvbuf, v.cols, per, v.rows, v.cols, nz, h.add, ctx->stream));
+        ++ctx->launches;
+      }
+    }
+  }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_appp_passes(ptycho_ctx ctx) {
+  PASS(need_ws(ctx));
+  CK(cudaSetDevice(ctx->device));
+  for (const Hop& h : ctx->hops) {
+    if (h.y1 <= h.y0 || h.x1 <= h.x0) continue;  // disjoint extended rects: empty message
+    const int so = ctx->tiles[h.src].owner, d = ctx->tiles[h.dst].owner;
+    if (so == ctx->rank && d == ctx->rank) PASS(hop_local(ctx, h));
+    else if (so == ctx->rank) PASS(hop_remote(ctx, h, true));
+    else if (d == ctx->rank) PASS(hop_remote(ctx, h, false));
+  }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_step(ptycho_ctx ctx) {
+  PASS(need_ws(ctx));
+  CK(cudaSetDevice(ctx->device));
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    CK(launch_acc_step(t.V, t.acc, (long long)t.slice_stride * ctx->cfg.slices, ctx->cfg.alpha_acc, ctx->stream));
+    ++ctx->launches;
+  }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_iterate(ptycho_ctx ctx, double* loss_out) {
+  PASS(need_run(ctx));
+  CK(cudaSetDevice(ctx->device));
+  size_t nmax = 0;
+  for (const Tile& t : ctx->tiles) nmax = std::max(nmax, t.probes.size());
+  if (nmax == 0) return PTYCHO_OK;
+  const int64_t T = ctx->cfg.pass_period > 0 ? ctx->cfg.pass_period : (int64_t)nmax;
+  const int64_t nseg = ((int64_t)nmax + T - 1) / T;
+  if (loss_out) PASS(zero_loss(ctx));
+  for (int64_t j = 0; j < nseg; ++j) {
+    PASS(run_probes(ctx, j * T, T, CHAIN_GRAD));
+    PASS(ptycho_appp_passes(ctx));
+    PASS(ptycho_step(ctx));
+  }
+  if (loss_out) {
+    double local = 0.0;
+    PASS(sum_loss(ctx, &local));
+    if (ctx->nranks > 1) {
+      CK(cudaMemcpyAsync(ctx->dscratch, &local, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      NK(ncclAllReduce(ctx->dscratch, ctx->dscratch, 1, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+      CK(cudaMemcpyAsync(&local, ctx->dscratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+    *loss_out = local;
+  }
+  return PTYCHO_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// stitch (Alg. 1 step 20)
+// ------------------------------------------------------------------------------------------
+extern "C" ptycho_status ptycho_stitch(ptycho_ctx ctx, float* V_out, int out_on_device, int32_t root) {
+  PASS(need_ws(ctx));
+  if (root < 0 || root >= ctx->nranks) return fail(ctx, PTYCHO_EARG, "bad root %d", root);
+  const bool am_root = ctx->rank == root;
+  if (am_root && !V_out) return fail(ctx, PTYCHO_EARG, "V_out is NULL on the root");
+  CK(cudaSetDevice(ctx->device));
+  const auto& cfg = ctx->cfg;
+  const size_t hw = (size_t)cfg.height * cfg.width;
+  for (int s = 0; s < cfg.slices; ++s) {
+    float* g = am_root ? (out_on_device ? V_out + (size_t)s * hw : ctx->staging) : nullptr;
+    for (const Tile& t : ctx->tiles) {
+      const int ih = t.iy1 - t.iy0, iw = t.ix1 - t.ix0;
+      if (t.owner == ctx->rank && am_root) {
+        PASS(tile_to_global(ctx, t, t.V, s, g, t.iy0, t.iy1, t.ix0, t.ix1));
+      } else if (t.owner == ctx->rank) {  // pack my interior [ih][iw] and send it to the root
+        float* tmp = ctx->sendbuf;
+        const float* sl = t.V + (long long)s * t.slice_stride;
+        if ((s & 1) == 0)
+          CK(launch_copy2d(tmp, iw, 0, sl + (long long)(t.iy0 - t.ey0) * t.pitch0 + (t.ix0 - t.ex0), t.pitch0, 0, ih, iw,
+                           1, 0, ctx->stream));
+        else
+          CK(launch_transpose2d(tmp, iw, 0, sl + (long long)(t.ix0 - t.ex0) * t.pitch1 + (t.iy0 - t.ey0), t.pitch1, 0,
+                                ih, iw, 1, 0, ctx->stream));
+        ++ctx->launches;
+        NK(ncclSend(tmp, (size_t)ih * iw, ncclFloat, root, ctx->comm, ctx->stream));
+      } else if (am_root) {
+        NK(ncclRecv(ctx->recvbuf, (size_t)ih * iw, ncclFloat, t.owner, ctx->comm, ctx->stream));
+        CK(launch_copy2d(g + (size_t)t.iy0 * cfg.width + t.ix0, cfg.width, 0, ctx->recvbuf, iw, 0, ih, iw, 1, 0,
+                         ctx->stream));
+        ++ctx->launches;
+      }
+    }
+    if (am_root && !out_on_device)
+      CK(cudaMemcpyAsync(V_out + (size_t)s * hw, ctx->staging, hw * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    if (am_root && !out_on_device) CK(cudaStreamSynchronize(ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_synchronize(ptycho_ctx ctx) {
+  if (!ctx) return PTYCHO_EARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int k : ctx->local)
+    if (ctx->tiles[k].stream) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_kernel_launches(ptycho_ctx ctx, int64_t* count) {
+  if (!ctx || !count) return PTYCHO_EARG;
+  *count = ctx->launches;
+  return PTYCHO_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// debug exports
+// ------------------------------------------------------------------------------------------
+static ptycho_status local_tile(ptycho_ctx ctx, int tile, Tile** out) {
+  if (tile < 0 || tile >= (int)ctx->tiles.size() || ctx->tiles[tile].owner != ctx->rank)
+    return fail(ctx, PTYCHO_EARG, "tile %d is not local", tile);
+  *out = &ctx->tiles[tile];
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_debug_read_tile(ptycho_ctx ctx, int32_t tile, int32_t which, float* out) {
+  PASS(need_ws(ctx));
+  Tile* t = nullptr;
+  PASS(local_tile(ctx, tile, &t));
+  if (!out) return fail(ctx, PTYCHO_EARG, "out is NULL");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int k : ctx->local) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
+  const float* buf = which ? t->acc : t->V;
+  const size_t area = (size_t)t->eh * t->ew;
+  for (int s = 0; s < ctx->cfg.slices; ++s) {
+    // staging viewed as [eh][ew]: use a private pitch = ew by calling the kernels directly
+    const float* sl = buf + (long long)s * t->slice_stride;
+    if ((s & 1) == 0) CK(launch_copy2d(ctx->staging, t->ew, 0, sl, t->pitch0, 0, t->eh, t->ew, 1, 0, ctx->stream));
+    else CK(launch_transpose2d(ctx->staging, t->ew, 0, sl, t->pitch1, 0, t->eh, t->ew, 1, 0, ctx->stream));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(out + s * area, ctx->staging, area * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_debug_write_tile(ptycho_ctx ctx, int32_t tile, int32_t which, const float* in) {
+  PASS(need_ws(ctx));
+  Tile* t = nullptr;
+  PASS(local_tile(ctx, tile, &t));
+  if (!in) return fail(ctx, PTYCHO_EARG, "in is NULL");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float* buf = which ? t->acc : t->V;
+  const size_t area = (size_t)t->eh * t->ew;
+  for (int s = 0; s < ctx->cfg.slices; ++s) {
+    float* sl = buf + (long long)s * t->slice_stride;
+    CK(cudaMemcpyAsync(ctx->staging, in + s * area, area * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    if ((s & 1) == 0) CK(launch_copy2d(sl, t->pitch0, 0, ctx->staging, t->ew, 0, t->eh, t->ew, 1, 0, ctx->stream));
+    else CK(launch_transpose2d(sl, t->pitch1, 0, ctx->staging, t->ew, 0, t->ew, t->eh, 1, 0, ctx->stream));
+    ++ctx->launches;
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return PTYCHO_OK;
+}
+
+static ptycho_status debug_chain(ptycho_ctx ctx, int tile, int64_t probe, ChainMode mode, Tile** tout) {
+  PASS(need_run(ctx));
+  Tile* t = nullptr;
+  PASS(local_tile(ctx, tile, &t));
+  if (probe < 0 || probe >= (int64_t)t->probes.size()) return fail(ctx, PTYCHO_EARG, "bad probe %lld", (long long)probe);
+  CK(cudaSetDevice(ctx->device));
+  PASS(zero_loss(ctx));
+  PASS(set_cursor(ctx, *t, (int)probe, ctx->stream));
+  PASS(enqueue_chain(ctx, *t, mode, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *tout = t;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_debug_probe_grad(ptycho_ctx ctx, int32_t tile, int64_t probe, float* grad_out,
+                                                 double* loss_out) {
+  Tile* t = nullptr;
+  PASS(debug_chain(ctx, tile, probe, CHAIN_DEBUG_GRAD, &t));
+  const size_t cnt = (size_t)ctx->cfg.slices * ctx->cfg.n * ctx->cfg.n;
+  if (grad_out) CK(cudaMemcpy(grad_out, ctx->debug, cnt * sizeof(float), cudaMemcpyDeviceToHost));
+  if (loss_out) PASS(sum_loss(ctx, loss_out));
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_debug_exit_wave(ptycho_ctx ctx, int32_t tile, int64_t probe, void* psi_out) {
+  Tile* t = nullptr;
+  PASS(debug_chain(ctx, tile, probe, CHAIN_DEBUG_EXIT, &t));
+  const size_t cnt = (size_t)ctx->cfg.n * ctx->cfg.n;
+  if (psi_out) CK(cudaMemcpy(psi_out, ctx->debug, cnt * sizeof(float2), cudaMemcpyDeviceToHost));
+  return PTYCHO_OK;
+}

@@ -1,0 +1,73 @@
+// Internal declarations shared by api.cu (host orchestration) and kernels.cu (sm_100a kernels).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace ptycho {
+
+// Lines (1-D transforms) handled by one CTA in a pass kernel.  The transposed store writes
+// LINES_PER_CTA consecutive complex64 (= 32 B, one L2 sector) per output row.
+constexpr int LINES_PER_CTA = 4;
+
+// Everything a pass kernel needs; passed by value (baked into the per-probe CUDA graph, the
+// probe index itself is read from *cursor on the device).
+struct PassArgs {
+  float* V;                 // V_k, slice s at V + s*slice_stride; layout L_{s&1}
+  float* acc;               // AccBuf_k, same layout as V
+  long long slice_stride;   // floats per slice
+  int pitch0, pitch1;       // row pitch of even slices ([eh][pitch0]) and odd slices ([ew][pitch1])
+  int ey0, ex0, eh, ew;     // R_k in global coordinates
+  float2* stash;            // phi_s, [S][N][N] in layout L_{s&1}
+  const float2* in;         // wavefield in (line-major in this pass's layout)
+  float2* out;              // wavefield out (written transposed)
+  const float2* probe;      // p, [N][N] natural
+  float* amp;               // measurement store [n_k][N][N], layout L_{S&1}, DC at [0][0]
+  const int2* centers;      // (cy, cx) of the tile's probes, local order
+  int* cursor;              // current local probe index (device)
+  unsigned* done;           // block-completion counter for the cursor advance
+  double* loss_part;        // per-CTA loss partial sums
+  const float2* wtab;       // W_N^k = exp(-2 pi i k/N), k < N (rounded from double)
+  const float2* htab;       // H_1[u]/N = exp(-i pi c m_u^2/N^2)/N (rounded from double)
+  float* gexport;           // debug: gradient out [S][N][N] natural (GRAD passes) or nullptr
+  float2* natural_out;      // debug: exit wave out [N][N] natural
+  float sigma, alpha, thr;  // t = exp(i sigma V); per-probe step; |Psi| threshold (true scale)
+  int s;                    // slice index of this pass (TRANSMIT / GRAD)
+  int advance;              // last block increments *cursor when done
+  int natural_transposed;   // debug store: lines are columns (1) or rows (0)
+};
+
+enum PassKind : int {
+  K_FWD_FIRST_PROP = 0,   // probe in; t_0; stash; P            ; store^T
+  K_FWD_FIRST_FFT,        // probe in; t_0; stash; FFT          ; store^T  (S == 1)
+  K_FWD_MID,              // P ; t_s ; stash ; P                 ; store^T
+  K_FWD_LAST,             // P ; t_s ; stash ; FFT               ; store^T
+  K_TURN,                 // FFT ; residual/loss/chi ; IFFT      ; store^T
+  K_SIMULATE,             // FFT ; write |X| to the measurement store
+  K_BWD_LAST_PROP,        // IFFT ; grad/update ; P^H            ; store^T  (s = S-1 > 0)
+  K_BWD_LAST_END,         // IFFT ; grad/update                  (S == 1)
+  K_BWD_MID,              // P^H ; grad/update ; P^H             ; store^T
+  K_BWD_END,              // P^H ; grad/update                   (s = 0)
+  K_EXIT_COMPLETE,        // P ; natural store (debug exit wave)
+  K_COUNT
+};
+
+// Launch one pass kernel (with programmatic dependent launch on `stream`).
+cudaError_t launch_pass(int n, PassKind kind, const PassArgs& a, cudaStream_t stream, bool pdl);
+
+// Region ops on per-slice alternating layouts.  dst/src are 2-D strided float arrays.
+//   op 0: dst = src ; op 1: dst += src
+cudaError_t launch_copy2d(float* dst, long long dld, long long dss, const float* src, long long sld,
+                          long long sss, int rows, int cols, int nslices, int op, cudaStream_t stream);
+// dst[r][c] (op)= src[c][r]  (transposing copy), slices as above
+cudaError_t launch_transpose2d(float* dst, long long dld, long long dss, const float* src, long long sld,
+                               long long sss, int rows, int cols, int nslices, int op, cudaStream_t stream);
+// V -= alpha*acc ; acc = 0  over n floats
+cudaError_t launch_acc_step(float* V, float* acc, long long n, float alpha, cudaStream_t stream);
+// measurement store: dst[c][.][.] from src[c][N][N] with ifftshift / sqrt / transpose options
+cudaError_t launch_amp_load(float* dst, const float* src, int count, int n, int shift, int intensity,
+                            int transpose, cudaStream_t stream);
+cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t stream);
+cudaError_t launch_sum_double(const double* parts, int n, double* out, cudaStream_t stream);
+
+}  // namespace ptycho

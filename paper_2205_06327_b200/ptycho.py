@@ -1,0 +1,255 @@
+"""Thin Python binding of include/ptycho.h (ctypes; argument marshalling only).
+
+Every step of the hot path runs in libptycho.so's sm_100a kernels.  There is no CPU or
+PyTorch fallback: if the extension is missing, importing this module raises.  PyTorch is used
+only for device memory (the workspace), streams and torch.distributed plumbing.
+
+The raw C entry points are exported under their C names (ptycho_create, ptycho_set_tiles, ...);
+the class `Ptycho` wraps them for tests and bench.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libptycho.so")
+
+PTYCHO_F_EXACT_WINDOW = 1
+PTYCHO_AMP_DC_CENTERED = 1
+PTYCHO_AMP_INTENSITY = 2
+STATUS = {0: "OK", 1: "EARG", 2: "ESHAPE", 3: "ESTATE", 4: "EHALO", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
+
+
+class ptycho_config(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("slices", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("width", ctypes.c_int32), ("sigma", ctypes.c_float), ("prop_c", ctypes.c_float),
+                ("alpha", ctypes.c_float), ("alpha_acc", ctypes.c_float), ("tau", ctypes.c_float),
+                ("pass_period", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(the CUDA extension is required; there is no fallback)")
+lib = ctypes.CDLL(LIB_PATH)
+
+_c = ctypes
+_P = _c.c_void_p
+_SIGS = {
+    "ptycho_create": [_c.POINTER(ptycho_config), _c.c_int, _P, _c.POINTER(_P)],
+    "ptycho_destroy": [_P],
+    "ptycho_nccl_unique_id": [_P, _c.c_size_t],
+    "ptycho_set_tiles": [_P, _c.c_int32, _c.c_int32, _c.c_int32, _P, _P, _c.c_int32, _c.c_int32],
+    "ptycho_set_scan": [_P, _P, _c.c_int64],
+    "ptycho_local_probes": [_P, _P, _c.POINTER(_c.c_int64)],
+    "ptycho_tile_probe_count": [_P, _c.c_int32, _c.POINTER(_c.c_int64)],
+    "ptycho_tile_rect": [_P, _c.c_int32, _P, _P],
+    "ptycho_workspace_bytes": [_P, _c.POINTER(_c.c_size_t)],
+    "ptycho_set_workspace": [_P, _P, _c.c_size_t],
+    "ptycho_set_probe": [_P, _P, _c.c_int],
+    "ptycho_load_measurements": [_P, _P, _c.c_int, _c.c_int64, _c.c_int64, _c.c_int32],
+    "ptycho_set_volume": [_P, _P, _c.c_int],
+    "ptycho_simulate_measurements": [_P],
+    "ptycho_forward_grad": [_P, _c.c_int64, _c.c_int64, _c.POINTER(_c.c_double)],
+    "ptycho_appp_passes": [_P],
+    "ptycho_step": [_P],
+    "ptycho_iterate": [_P, _c.POINTER(_c.c_double)],
+    "ptycho_stitch": [_P, _P, _c.c_int, _c.c_int32],
+    "ptycho_synchronize": [_P],
+    "ptycho_kernel_launches": [_P, _c.POINTER(_c.c_int64)],
+    "ptycho_debug_read_tile": [_P, _c.c_int32, _c.c_int32, _P],
+    "ptycho_debug_write_tile": [_P, _c.c_int32, _c.c_int32, _P],
+    "ptycho_debug_probe_grad": [_P, _c.c_int32, _c.c_int64, _P, _c.POINTER(_c.c_double)],
+    "ptycho_debug_exit_wave": [_P, _c.c_int32, _c.c_int64, _P],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _c.c_int
+    globals()[_name] = _f
+lib.ptycho_last_error.argtypes = [_P]
+lib.ptycho_last_error.restype = _c.c_char_p
+ptycho_last_error = lib.ptycho_last_error
+
+EXPORTED = sorted(list(_SIGS) + ["ptycho_last_error"])
+
+
+class PtychoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(a):
+    """Device pointer of a torch tensor or host pointer of a contiguous numpy array."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _on_device(a):
+    return 0 if (a is None or isinstance(a, np.ndarray)) else int(a.is_cuda)
+
+
+class Ptycho:
+    """One context = one rank's share of the reconstruction (ptycho_create ... ptycho_destroy)."""
+
+    def __init__(self, n, slices, height, width, sigma=0.1, prop_c=3.135, alpha=1.0, alpha_acc=None,
+                 tau=1e-4, pass_period=0, flags=0, device=0, stream=None):
+        import torch
+        self.torch = torch
+        self.cfg = ptycho_config(n, slices, height, width, sigma, prop_c, alpha,
+                                 alpha if alpha_acc is None else alpha_acc, tau, pass_period, flags)
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        self.stream = stream
+        h = _P()
+        st = lib.ptycho_create(ctypes.byref(self.cfg), device, _P(stream), ctypes.byref(h))
+        if st != 0:
+            raise PtychoError(st, lib.ptycho_last_error(None).decode())
+        self.h = h
+        self.workspace = None
+
+    def _ck(self, st):
+        if st != 0:
+            raise PtychoError(st, lib.ptycho_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ptycho_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        st = lib.ptycho_nccl_unique_id(buf, 128)
+        if st != 0:
+            raise PtychoError(st, lib.ptycho_last_error(None).decode())
+        return buf.raw
+
+    def set_tiles(self, rows, cols, halo, tile_owner=None, nccl_id=None, rank=0, nranks=1):
+        own = None if tile_owner is None else np.ascontiguousarray(tile_owner, dtype=np.int32)
+        nid = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
+        self._own = own
+        self._ck(lib.ptycho_set_tiles(self.h, rows, cols, halo, _ptr(own), nid, rank, nranks))
+        self.rows, self.cols = rows, cols
+
+    def set_scan(self, centers):
+        self._centers = np.ascontiguousarray(centers, dtype=np.int32)
+        self._ck(lib.ptycho_set_scan(self.h, self._centers.ctypes.data, len(self._centers)))
+
+    def local_probes(self):
+        cnt = ctypes.c_int64()
+        self._ck(lib.ptycho_local_probes(self.h, None, ctypes.byref(cnt)))
+        ids = np.zeros(cnt.value, dtype=np.int64)
+        self._ck(lib.ptycho_local_probes(self.h, ids.ctypes.data, ctypes.byref(cnt)))
+        return ids
+
+    def tile_probe_count(self, tile):
+        cnt = ctypes.c_int64()
+        self._ck(lib.ptycho_tile_probe_count(self.h, tile, ctypes.byref(cnt)))
+        return cnt.value
+
+    def tile_rect(self, tile):
+        ext = np.zeros(4, np.int32)
+        inter = np.zeros(4, np.int32)
+        self._ck(lib.ptycho_tile_rect(self.h, tile, ext.ctypes.data, inter.ctypes.data))
+        return tuple(int(v) for v in ext), tuple(int(v) for v in inter)
+
+    def workspace_bytes(self):
+        b = ctypes.c_size_t()
+        self._ck(lib.ptycho_workspace_bytes(self.h, ctypes.byref(b)))
+        return b.value
+
+    def allocate_workspace(self):
+        nbytes = self.workspace_bytes()
+        self.workspace = self.torch.empty(nbytes + 256, dtype=self.torch.uint8, device=f"cuda:{self.device}")
+        base = self.workspace.data_ptr()
+        off = (-base) % 256
+        self._ck(lib.ptycho_set_workspace(self.h, base + off, nbytes))
+        return nbytes
+
+    def set_probe(self, probe):
+        if isinstance(probe, np.ndarray):
+            probe = np.ascontiguousarray(probe, dtype=np.complex64)
+        self._ck(lib.ptycho_set_probe(self.h, _ptr(probe), _on_device(probe)))
+
+    def load_measurements(self, amp, first_local=0, flags=0):
+        if isinstance(amp, np.ndarray):
+            amp = np.ascontiguousarray(amp, dtype=np.float32)
+        self._ck(lib.ptycho_load_measurements(self.h, _ptr(amp), _on_device(amp), first_local, len(amp), flags))
+
+    def set_volume(self, volume=None):
+        if isinstance(volume, np.ndarray):
+            volume = np.ascontiguousarray(volume, dtype=np.float32)
+        self._ck(lib.ptycho_set_volume(self.h, _ptr(volume), _on_device(volume)))
+
+    def simulate_measurements(self):
+        self._ck(lib.ptycho_simulate_measurements(self.h))
+
+    def forward_grad(self, first, count, want_loss=False):
+        loss = ctypes.c_double()
+        self._ck(lib.ptycho_forward_grad(self.h, first, count, ctypes.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
+    def appp_passes(self):
+        self._ck(lib.ptycho_appp_passes(self.h))
+
+    def step(self):
+        self._ck(lib.ptycho_step(self.h))
+
+    def iterate(self, want_loss=False):
+        loss = ctypes.c_double()
+        self._ck(lib.ptycho_iterate(self.h, ctypes.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
+    def stitch(self, out=None, root=0, rank=0):
+        c = self.cfg
+        if out is None and rank == root:
+            out = np.zeros((c.slices, c.height, c.width), np.float32)
+        self._ck(lib.ptycho_stitch(self.h, _ptr(out), _on_device(out), root))
+        return out
+
+    def synchronize(self):
+        self._ck(lib.ptycho_synchronize(self.h))
+
+    def kernel_launches(self):
+        v = ctypes.c_int64()
+        self._ck(lib.ptycho_kernel_launches(self.h, ctypes.byref(v)))
+        return v.value
+
+    # ---- debug exports
+    def debug_read_tile(self, tile, which):
+        ext, _ = self.tile_rect(tile)
+        out = np.zeros((self.cfg.slices, ext[2] - ext[0], ext[3] - ext[1]), np.float32)
+        self._ck(lib.ptycho_debug_read_tile(self.h, tile, which, out.ctypes.data))
+        return out
+
+    def debug_write_tile(self, tile, which, arr):
+        arr = np.ascontiguousarray(arr, dtype=np.float32)
+        self._ck(lib.ptycho_debug_write_tile(self.h, tile, which, arr.ctypes.data))
+
+    def debug_probe_grad(self, tile, probe):
+        n, s = self.cfg.n, self.cfg.slices
+        g = np.zeros((s, n, n), np.float32)
+        loss = ctypes.c_double()
+        self._ck(lib.ptycho_debug_probe_grad(self.h, tile, probe, g.ctypes.data, ctypes.byref(loss)))
+        return g, loss.value
+
+    def debug_exit_wave(self, tile, probe):
+        n = self.cfg.n
+        psi = np.zeros((n, n), np.complex64)
+        self._ck(lib.ptycho_debug_exit_wave(self.h, tile, probe, psi.ctypes.data))
+        return psi
