@@ -1,0 +1,328 @@
+"""Benchmark of the gradient-decomposition hot path (arXiv 2205.06327) on B200.
+
+A step = one reconstruction iteration ("a cycle through all the probe locations") of the
+LT-small-shaped workload (BASELINE.json configs[3]: 1024x1024x4158 synthetic measurements,
+1536x1536x100 object) over the fixed 2x4 tile grid (halo N/2, exact window), tiles spread over
+the ranks (8/N virtual tiles per GPU): per-probe forward + adjoint gradient + AccBuf scatter-add
++ SGD for every probe, the four APPP passes, the accumulated step.  Total work is fixed as N
+grows ("scaling": "strong"); results are bit-identical for every N.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (contract in the task statement).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "probe-locations/sec and sec/iteration at 1/2/4/8 B200; % HBM peak"
+PAPER_BEST_LT_SMALL = 2310.0  # probe-locations/s, GD on 462 V100s (Table II(a))
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and not s[2 + i].startswith("Not")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_oracle_sample(cfg, probe, vt, centers, n_probes=1):
+    """The float64 oracle, as it stands, on a bounded sample: the full forward + adjoint gradient
+    of `n_probes` probes of the workload (N=1024, S=100).  Returns (probes/s, seconds, sample)."""
+    from oracle import ptycho_oracle as O
+    full = (0, 0, cfg.height, cfg.width)
+    i0 = len(centers) // 2
+    t0 = time.perf_counter()
+    for i in range(i0, i0 + n_probes):
+        c = tuple(int(v) for v in centers[i])
+        vwin = O.window(vt, full, c, cfg.n).astype(np.float64)
+        amp = np.abs(np.fft.fft2(probe, norm="ortho"))  # any non-negative amplitude: timing is data-independent
+        O.probe_grad(probe, vwin * 0.5, amp, cfg.sigma, cfg.prop_c)
+    dt = time.perf_counter() - t0
+    return n_probes / dt, dt, f"{n_probes} probe(s) of {cfg.name} (N={cfg.n}, S={cfg.slices}) forward+adjoint, float64"
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    probe = synth.probe(cfg.n, cfg.defocus_nm)
+    vt = synth.volume(0, cfg.slices, cfg.height, cfg.width)
+    centers = synth.scan_centers(cfg.height, cfg.width, cfg.scan_ny, cfg.scan_nx)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(cfg, probe, vt, centers, 1)
+    times = []
+    for _ in range(args.steps):
+        _, dt, sample = cpu_oracle_sample(cfg, probe, vt, centers, 1)
+        times.append(dt)
+    sec = sum(times) / len(times)
+    value = 1.0 / sec
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "probe-locations/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": value / PAPER_BEST_LT_SMALL,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "sample": "1 probe per step (bounded sample of the iteration)"},
+            "cpu_baseline": {"value": value, "unit": "probe-locations/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "probe-locations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def interior_run(p, tile, centers, n, h, w, want=4):
+    """first local index of `want` consecutive probes of `tile` whose windows lie inside the object"""
+    cnt = p.tile_probe_count(tile)
+    # tile's own probes in ascending global order = local_probes restricted to the tile
+    ids = [i for i in p.local_probes() if _tile_of(p, i, centers)[0] == tile]
+    run = 0
+    for j, g in enumerate(ids):
+        cy, cx = centers[g]
+        ok = cy - n // 2 >= 0 and cy + n // 2 <= h and cx - n // 2 >= 0 and cx + n // 2 <= w
+        run = run + 1 if ok else 0
+        if run == want:
+            return j - want + 1
+    return 0 if cnt >= want else None
+
+
+def _tile_of(p, g, centers):
+    cy, cx = centers[g]
+    for k in range(p.rows * p.cols):
+        _, (y0, x0, y1, x1) = p.tile_rect(k)
+        if y0 <= cy < y1 and x0 <= cx < x1:
+            return k, None
+    return -1, None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="lt_small")
+    ap.add_argument("--grid", default=None, help="tile grid RxC (default: the config's, 2x4)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2205_06327_b200.ptycho import Ptycho
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    cfg = synth.CONFIGS[args.config]
+    R, C = (int(v) for v in args.grid.split("x")) if args.grid else cfg.grid
+    ntiles = R * C
+    owner = [k * world // ntiles for k in range(ntiles)]
+    nid = None
+    if world > 1:
+        obj = [Ptycho.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    n, S, H, W = cfg.n, cfg.slices, cfg.height, cfg.width
+    alpha = 0.5
+    stream = torch.cuda.Stream(local_rank)
+    p = Ptycho(n, S, H, W, cfg.sigma, cfg.prop_c, alpha=alpha, device=local_rank, stream=stream.cuda_stream)
+    p.set_tiles(R, C, n // 2, owner, nid, rank, world)
+    centers = synth.scan_centers(H, W, cfg.scan_ny, cfg.scan_nx)
+    p.set_scan(centers)
+    ws = p.allocate_workspace()
+    probe = synth.probe(n, cfg.defocus_nm)
+    p.set_probe(probe.astype(np.complex64))
+    vt = synth.volume(0, S, H, W)
+    p.set_volume(vt)
+    p.simulate_measurements()          # a_i = |G(p_i, V_true)| on the device
+    p.set_volume(None)                 # V_0 = 0
+    p.synchronize()
+    nloc = len(p.local_probes())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        p.iterate()
+    barrier()
+    l0 = p.kernel_launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            p.iterate()
+        e1.record(stream)
+        p.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = p.kernel_launches() - l0
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        lt = torch.tensor([launches], dtype=torch.int64, device="cuda")
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    value = cfg.n_probes / (ms / 1e3)
+    loss = p.iterate(want_loss=True)   # F(V) after K+W+1 iterations (untimed; sanity)
+
+    # ---- roofline of the dominant kernel (backward middle pass), CUDA events on its stream
+    peak, peak_kind = hbm_peak()
+    my_tiles = [k for k in range(ntiles) if owner[k] == rank]
+    tile = my_tiles[len(my_tiles) // 2]
+    j0 = interior_run(p, tile, centers, n, H, W)
+    prof = p.profile_chain(tile, j0 or 0, 4) if j0 is not None else {}
+    n2 = n * n
+    bwd = prof.get("bwd_mid", (0.0, 0))
+    fwd = prof.get("fwd_mid", (0.0, 0))
+    chain_ms = sum(v[0] for v in prof.values())
+    t_bwd = bwd[0] / max(bwd[1], 1) * 1e-3
+    t_fwd = fwd[0] / max(fwd[1], 1) * 1e-3
+    bytes_bwd = 24 * n2   # stash read 8N^2 + V rmw 8N^2 + AccBuf rmw 8N^2 (algorithmic, per launch)
+    bytes_fwd = 12 * n2   # V read 4N^2 + stash write 8N^2
+    achieved = bytes_bwd / t_bwd / 1e9 if t_bwd > 0 else None
+    traffic = None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = summ.get("bwd_mid", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    flops_pass = 4 * 5 * n * np.log2(n) * n  # nominal 5 n log2 n per 1-D transform, 4 transforms per line
+    roofline = {"bound": "hbm", "kernel": "pass_kernel<1024, bwd_mid> (P^H, grad/AccBuf/SGD, P^H)",
+                "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": bytes_bwd,
+                "ms_per_launch": t_bwd * 1e3,
+                "share_of_chain": bwd[0] / chain_ms if chain_ms else None,
+                "fwd_mid": {"ms_per_launch": t_fwd * 1e3, "achieved_gbs": bytes_fwd / t_fwd / 1e9 if t_fwd else None,
+                            "fp32_tflops_nominal": flops_pass / t_fwd / 1e12 if t_fwd else None},
+                "chain_ms_per_probe_isolated": chain_ms / 4 if chain_ms else None}
+
+    # ---- e2e: host measurements (pinned) -> device, one iteration, stitched V -> host, each step
+    e2e = None
+    if not args.no_e2e:
+        host_amp = torch.empty((nloc, n, n), dtype=torch.float32, pin_memory=True)
+        p.read_measurements(0, nloc, host_amp)
+        host_v = torch.empty((S, H, W), dtype=torch.float32, pin_memory=True) if rank == 0 else None
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            p.load_measurements(host_amp)
+            p.iterate()
+            p.stitch(host_v, root=0, rank=rank)
+        f1.record(stream)
+        p.synchronize()
+        barrier()
+        ems = f0.elapsed_time(f1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": cfg.n_probes / (ems / 1e3), "unit": "probe-locations/s",
+               "h2d_bytes_per_step": cfg.n_probes * n2 * 4, "d2h_bytes_per_step": S * H * W * 4,
+               "ms_per_step": ems, "steps": args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, dt, sample = cpu_oracle_sample(cfg, probe, vt, centers, 1)
+        cpu = {"value": v, "unit": "probe-locations/s", "cores": 1, "kind": "oracle", "sample": sample,
+               "seconds": dt}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "probe-locations/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "sec_per_iteration": ms / 1e3,
+                "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": value / PAPER_BEST_LT_SMALL, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{cfg.name}: {n}x{n}x{cfg.n_probes} measurements, {W}x{H}x{S} object",
+                           "grid": f"{R}x{C}", "halo": n // 2, "tiles_per_gpu": ntiles // world,
+                           "alpha": alpha, "pass_period": "once per iteration",
+                           "l2": "inputs > L2 (V_k+AccBuf 8.9 GB, |y| 17.4 GB)",
+                           "workspace_gb_per_gpu": ws / 1e9},
+                "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
+                "e2e": e2e, "cpu_baseline": cpu, "loss_after": loss,
+                "paper_context": "GD small LT: 2310 probe-locations/s on 462 V100 (P:65-74)"}
+        print(json.dumps(line), flush=True)
+    p.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,11 @@ ptycho_status ptycho_set_probe(ptycho_ctx ctx, const void* probe_c64, int on_dev
 ptycho_status ptycho_load_measurements(ptycho_ctx ctx, const float* amp, int on_device,
                                        int64_t first_local, int64_t count, int32_t layout_flags);
 
+/* Inverse of load_measurements: copy the stored amplitudes of local probes [first_local,
+ * first_local+count) to host float32 [count][N][N], DC at [0][0] (e.g. after
+ * simulate_measurements).  Synchronizes. */
+ptycho_status ptycho_read_measurements(ptycho_ctx ctx, float* amp_out, int64_t first_local, int64_t count);
+
 /* Alg. 1 step 3: every local tile receives V on R_k from the global volume
  * float32 [S][H][W] (host or device); V == NULL sets V_0 = 0.  AccBuf_k is zeroed. */
 ptycho_status ptycho_set_volume(ptycho_ctx ctx, const float* volume, int on_device);
@@ -186,6 +191,15 @@ ptycho_status ptycho_synchronize(ptycho_ctx ctx);
 
 /* Number of kernels this context has launched so far (all streams, including graph nodes). */
 ptycho_status ptycho_kernel_launches(ptycho_ctx ctx, int64_t* count);
+
+/* Measurement export (bench.py roofline): run the pass chain of local probes [first, first+count)
+ * of local tile `tile` (real work: V_k and AccBuf_k are updated exactly as by forward_grad) with
+ * direct launches bracketed by CUDA events on the tile's stream, and return per pass kind
+ * (0..10, see PassKind in csrc/internal.h: 2 = forward middle pass, 8 = backward middle pass)
+ * the summed kernel time in ms and the number of launches.  ms_out / launches_out: [11].
+ * Synchronizes. */
+ptycho_status ptycho_profile_chain(ptycho_ctx ctx, int32_t tile, int64_t first, int64_t count, double* ms_out,
+                                   int64_t* launches_out);
 
 /* ---------------------------------------------------------------------------------------------
  * Debug exports (same library; used by the parity tests).  All synchronize; host buffers.

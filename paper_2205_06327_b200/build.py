@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     for p in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
-    link = [nvcc, "-shared", "-o", LIB] + objs + ["-L", libdir, "-l:libnccl.so.2",
+    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-L", libdir, "-l:libnccl.so.2",
                                                     "-Xlinker", "-rpath=" + libdir, "--cudart", "static"]
     if verbose:
         print(" ".join(link), flush=True)

@@ -511,6 +511,38 @@ extern "C" ptycho_status ptycho_load_measurements(ptycho_ctx ctx, const float* a
   return PTYCHO_OK;
 }
 
+extern "C" ptycho_status ptycho_read_measurements(ptycho_ctx ctx, float* amp_out, int64_t first_local,
+                                                  int64_t count) {
+  PASS(need_ws(ctx));
+  int64_t nloc = 0;
+  for (int k : ctx->local) nloc += (int64_t)ctx->tiles[k].probes.size();
+  if (count < 0 || first_local < 0 || first_local + count > nloc) return fail(ctx, PTYCHO_EARG, "bad range");
+  if (count == 0) return PTYCHO_OK;
+  if (!amp_out) return fail(ctx, PTYCHO_EARG, "amp_out is NULL");
+  CK(cudaSetDevice(ctx->device));
+  for (int k : ctx->local) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
+  const int n = ctx->cfg.n;
+  const size_t n2 = (size_t)n * n;
+  const int64_t chunk = (int64_t)(ctx->staging_floats / n2);
+  int64_t g = 0;
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const int64_t nk = (int64_t)t.probes.size();
+    const int64_t lo = std::max(first_local, g), hi = std::min(first_local + count, g + nk);
+    for (int64_t p = lo; p < hi;) {
+      const int64_t m = std::min(chunk, hi - p);
+      CK(launch_amp_load(ctx->staging, t.amp + (size_t)(p - g) * n2, (int)m, n, 0, 0, ctx->cfg.slices & 1, ctx->stream));
+      ++ctx->launches;
+      CK(cudaMemcpyAsync(amp_out + (size_t)(p - first_local) * n2, ctx->staging, (size_t)m * n2 * sizeof(float),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      p += m;
+    }
+    g += nk;
+  }
+  return PTYCHO_OK;
+}
+
 // slice pointers / region helpers for the alternating per-slice layout
 struct SliceView {
   float* base;       // first element of the region in the first slice of this parity
@@ -623,7 +655,13 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   return a;
 }
 
-static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cudaStream_t st) {
+struct ChainProfile {  // optional per-kind event timing (ptycho_profile_chain)
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> kind;
+};
+
+static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cudaStream_t st,
+                                   ChainProfile* prof = nullptr) {
   const int S = ctx->cfg.slices, n = ctx->cfg.n;
   PassArgs a = base_args(ctx, t);
   int pass = 0;
@@ -638,7 +676,19 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
       b.natural_out = (float2*)ctx->debug;
       b.natural_transposed = S & 1;
     }
-    CK(launch_pass(n, kind, b, st, ctx->use_pdl));
+    if (prof) {
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, st));
+      CK(launch_pass(n, kind, b, st, false));
+      CK(cudaEventRecord(e1, st));
+      prof->ev.push_back(e0);
+      prof->ev.push_back(e1);
+      prof->kind.push_back((int)kind);
+    } else {
+      CK(launch_pass(n, kind, b, st, ctx->use_pdl));
+    }
     ++ctx->launches;
     ++pass;
     return PTYCHO_OK;
@@ -1015,5 +1065,34 @@ extern "C" ptycho_status ptycho_debug_exit_wave(ptycho_ctx ctx, int32_t tile, in
   PASS(debug_chain(ctx, tile, probe, CHAIN_DEBUG_EXIT, &t));
   const size_t cnt = (size_t)ctx->cfg.n * ctx->cfg.n;
   if (psi_out) CK(cudaMemcpy(psi_out, ctx->debug, cnt * sizeof(float2), cudaMemcpyDeviceToHost));
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_profile_chain(ptycho_ctx ctx, int32_t tile, int64_t first, int64_t count,
+                                              double* ms_out, int64_t* launches_out) {
+  PASS(need_run(ctx));
+  Tile* t = nullptr;
+  PASS(local_tile(ctx, tile, &t));
+  if (!ms_out || !launches_out) return fail(ctx, PTYCHO_EARG, "outputs are NULL");
+  CK(cudaSetDevice(ctx->device));
+  for (int k = 0; k < K_COUNT; ++k) {
+    ms_out[k] = 0.0;
+    launches_out[k] = 0;
+  }
+  const int64_t nk = (int64_t)t->probes.size();
+  const int64_t m = std::max<int64_t>(0, std::min(first + count, nk) - first);
+  if (m == 0) return PTYCHO_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  PASS(set_cursor(ctx, *t, (int)first, t->stream));
+  ChainProfile prof;
+  for (int64_t j = 0; j < m; ++j) PASS(enqueue_chain(ctx, *t, CHAIN_GRAD, t->stream, &prof));
+  CK(cudaStreamSynchronize(t->stream));
+  for (size_t i = 0; i < prof.kind.size(); ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, prof.ev[2 * i], prof.ev[2 * i + 1]));
+    ms_out[prof.kind[i]] += ms;
+    launches_out[prof.kind[i]] += 1;
+  }
+  for (cudaEvent_t e : prof.ev) cudaEventDestroy(e);
   return PTYCHO_OK;
 }

@@ -50,6 +50,7 @@ _SIGS = {
     "ptycho_set_workspace": [_P, _P, _c.c_size_t],
     "ptycho_set_probe": [_P, _P, _c.c_int],
     "ptycho_load_measurements": [_P, _P, _c.c_int, _c.c_int64, _c.c_int64, _c.c_int32],
+    "ptycho_read_measurements": [_P, _P, _c.c_int64, _c.c_int64],
     "ptycho_set_volume": [_P, _P, _c.c_int],
     "ptycho_simulate_measurements": [_P],
     "ptycho_forward_grad": [_P, _c.c_int64, _c.c_int64, _c.POINTER(_c.c_double)],
@@ -59,6 +60,7 @@ _SIGS = {
     "ptycho_stitch": [_P, _P, _c.c_int, _c.c_int32],
     "ptycho_synchronize": [_P],
     "ptycho_kernel_launches": [_P, _c.POINTER(_c.c_int64)],
+    "ptycho_profile_chain": [_P, _c.c_int32, _c.c_int64, _c.c_int64, _P, _P],
     "ptycho_debug_read_tile": [_P, _c.c_int32, _c.c_int32, _P],
     "ptycho_debug_write_tile": [_P, _c.c_int32, _c.c_int32, _P],
     "ptycho_debug_probe_grad": [_P, _c.c_int32, _c.c_int64, _P, _c.POINTER(_c.c_double)],
@@ -191,6 +193,15 @@ class Ptycho:
             amp = np.ascontiguousarray(amp, dtype=np.float32)
         self._ck(lib.ptycho_load_measurements(self.h, _ptr(amp), _on_device(amp), first_local, len(amp), flags))
 
+    def read_measurements(self, first_local=0, count=None, out=None):
+        if count is None:
+            count = len(self.local_probes()) - first_local
+        n = self.cfg.n
+        if out is None:
+            out = np.zeros((count, n, n), np.float32)
+        self._ck(lib.ptycho_read_measurements(self.h, _ptr(out), first_local, count))
+        return out
+
     def set_volume(self, volume=None):
         if isinstance(volume, np.ndarray):
             volume = np.ascontiguousarray(volume, dtype=np.float32)
@@ -229,6 +240,15 @@ class Ptycho:
         v = ctypes.c_int64()
         self._ck(lib.ptycho_kernel_launches(self.h, ctypes.byref(v)))
         return v.value
+
+    PASS_KINDS = ["fwd_first_prop", "fwd_first_fft", "fwd_mid", "fwd_last", "turn", "simulate",
+                  "bwd_last_prop", "bwd_last_end", "bwd_mid", "bwd_end", "exit_complete"]
+
+    def profile_chain(self, tile, first, count):
+        ms = np.zeros(11, np.float64)
+        cnt = np.zeros(11, np.int64)
+        self._ck(lib.ptycho_profile_chain(self.h, tile, first, count, ms.ctypes.data, cnt.ctypes.data))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PASS_KINDS) if cnt[i]}
 
     # ---- debug exports
     def debug_read_tile(self, tile, which):
