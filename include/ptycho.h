@@ -105,6 +105,18 @@ ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t cols, int32
                                const int32_t* tile_owner, const void* nccl_id, int32_t rank,
                                int32_t nranks);
 
+/* Host-only geometry (no context, no GPU): rects[8*k .. 8*k+8) = {ext y0,x0,y1,x1, interior
+ * y0,x0,y1,x1} of tile k = r*C + c for the grid set_tiles would build (same code). */
+ptycho_status ptycho_tile_geometry(int32_t height, int32_t width, int32_t rows, int32_t cols, int32_t halo,
+                                   int32_t* rects);
+
+/* Host-only APPP schedule (no context, no GPU): the hop list appp_passes executes, in the global
+ * order every rank follows.  hops_out[7*i ..] = {src tile, dst tile, y0, y1, x0, x1, add (1 = ADD,
+ * forward passes; 0 = REPLACE, backward passes)}; hops_out may be NULL to query *count.
+ * 2(R-1)C + 2(C-1)R hops (some may have empty regions when extended rects do not meet). */
+ptycho_status ptycho_appp_schedule(int32_t height, int32_t width, int32_t rows, int32_t cols, int32_t halo,
+                                   int32_t* hops_out, int32_t max_hops, int32_t* count);
+
 /* Probe locations (raster order): host int32 [n_probes][2] = (cy, cx), global
  * order = acquisition time order.  Windows are N x N with top-left (cy-N/2, cx-N/2)
  * (reading #10); windows past the object edge are legal (V = 0 there, reading #12).  Probes

@@ -165,9 +165,13 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   const int n = cfg->n;
   ctx->h_wtab.resize(n);
   ctx->h_htab.resize(n);
+  const int Q = (int)std::lround(std::sqrt((double)n));  // N = P*Q with P = Q (kernels.cu Geo<N>)
+  for (int k = 0; k < n / Q; ++k)
+    for (int q = 0; q < Q; ++q) {  // four-step twiddle W_N^{qk}, stored [k][q] (coalesced per line)
+      const double th = -2.0 * M_PI * (double)(q * k) / (double)n;
+      ctx->h_wtab[k * Q + q] = make_float2((float)std::cos(th), (float)std::sin(th));
+    }
   for (int k = 0; k < n; ++k) {
-    const double th = -2.0 * M_PI * (double)k / (double)n;
-    ctx->h_wtab[k] = make_float2((float)std::cos(th), (float)std::sin(th));
     const double m = (k < n / 2) ? (double)k : (double)(k - n);
     const double ph = -M_PI * (double)cfg->prop_c * m * m / ((double)n * (double)n);
     ctx->h_htab[k] = make_float2((float)(std::cos(ph) / n), (float)(std::sin(ph) / n));
@@ -212,13 +216,105 @@ static void split(int extent, int parts, int p, int* a, int* b) {
   *b = (p == parts - 1) ? extent : (p + 1) * base;
 }
 
+// APPP hop list in the global order every rank follows (Fig. forward_backward a-d):
+// vertical forward (ADD down each tile column), vertical backward (REPLACE up), horizontal forward
+// and backward along each tile row over the full extended height Y_r (reading #21).
+static void build_hops(const std::vector<Tile>& tiles, int rows, int cols, std::vector<Hop>& hops) {
+  auto T = [&](int r, int c) -> const Tile& { return tiles[r * cols + c]; };
+  hops.clear();
+  for (int c = 0; c < cols; ++c)
+    for (int r = 0; r + 1 < rows; ++r) {
+      const Tile &a = T(r, c), &b = T(r + 1, c);
+      hops.push_back({a.k, b.k, std::max(a.ey0, b.ey0), std::min(a.ey1, b.ey1), a.ex0, a.ex1, 1});
+    }
+  for (int c = 0; c < cols; ++c)
+    for (int r = rows - 1; r >= 1; --r) {
+      const Tile &a = T(r, c), &b = T(r - 1, c);
+      hops.push_back({a.k, b.k, std::max(a.ey0, b.ey0), std::min(a.ey1, b.ey1), a.ex0, a.ex1, 0});
+    }
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c + 1 < cols; ++c) {
+      const Tile &a = T(r, c), &b = T(r, c + 1);
+      hops.push_back({a.k, b.k, a.ey0, a.ey1, std::max(a.ex0, b.ex0), std::min(a.ex1, b.ex1), 1});
+    }
+  for (int r = 0; r < rows; ++r)
+    for (int c = cols - 1; c >= 1; --c) {
+      const Tile &a = T(r, c), &b = T(r, c - 1);
+      hops.push_back({a.k, b.k, a.ey0, a.ey1, std::max(a.ex0, b.ex0), std::min(a.ex1, b.ex1), 0});
+    }
+}
+
+// Tile rects (readings #13, #14): uniform split, remainder to the last row /
+// column, extended rect = interior dilated by halo and clipped to the object.
+static void build_tiles(int height, int width, int rows, int cols, int halo, std::vector<Tile>& tiles) {
+  tiles.assign(rows * cols, Tile());
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) {
+      Tile& t = tiles[r * cols + c];
+      t.k = r * cols + c;
+      t.r = r;
+      t.c = c;
+      split(height, rows, r, &t.iy0, &t.iy1);
+      split(width, cols, c, &t.ix0, &t.ix1);
+      t.ey0 = std::max(0, t.iy0 - halo);
+      t.ex0 = std::max(0, t.ix0 - halo);
+      t.ey1 = std::min(height, t.iy1 + halo);
+      t.ex1 = std::min(width, t.ix1 + halo);
+      t.eh = t.ey1 - t.ey0;
+      t.ew = t.ex1 - t.ex0;
+      t.pitch0 = (t.ew + 31) / 32 * 32;
+      t.pitch1 = (t.eh + 31) / 32 * 32;
+      const long long a = (long long)t.eh * t.pitch0, b = (long long)t.ew * t.pitch1;
+      t.slice_stride = (std::max(a, b) + 31) / 32 * 32;
+    }
+}
+
+static bool grid_ok(int height, int width, int rows, int cols, int halo) {
+  return rows >= 1 && cols >= 1 && rows <= height && cols <= width && halo >= 0;
+}
+
+extern "C" ptycho_status ptycho_tile_geometry(int32_t height, int32_t width, int32_t rows, int32_t cols,
+                                              int32_t halo, int32_t* rects) {
+  ptycho_ctx ctx = nullptr;
+  if (!grid_ok(height, width, rows, cols, halo) || !rects) return fail(ctx, PTYCHO_EARG, "bad grid");
+  std::vector<Tile> tiles;
+  build_tiles(height, width, rows, cols, halo, tiles);
+  for (const Tile& t : tiles) {
+    int32_t* o = rects + 8 * t.k;
+    o[0] = t.ey0; o[1] = t.ex0; o[2] = t.ey1; o[3] = t.ex1;
+    o[4] = t.iy0; o[5] = t.ix0; o[6] = t.iy1; o[7] = t.ix1;
+  }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_appp_schedule(int32_t height, int32_t width, int32_t rows, int32_t cols,
+                                              int32_t halo, int32_t* hops_out, int32_t max_hops,
+                                              int32_t* count) {
+  ptycho_ctx ctx = nullptr;
+  if (!grid_ok(height, width, rows, cols, halo) || !count) return fail(ctx, PTYCHO_EARG, "bad grid");
+  std::vector<Tile> tiles;
+  std::vector<Hop> hops;
+  build_tiles(height, width, rows, cols, halo, tiles);
+  build_hops(tiles, rows, cols, hops);
+  *count = (int32_t)hops.size();
+  if (hops_out) {
+    if (max_hops < (int32_t)hops.size()) return fail(ctx, PTYCHO_EARG, "max_hops < %zu", hops.size());
+    for (size_t i = 0; i < hops.size(); ++i) {
+      const Hop& h = hops[i];
+      int32_t* o = hops_out + 7 * i;
+      o[0] = h.src; o[1] = h.dst; o[2] = h.y0; o[3] = h.y1; o[4] = h.x0; o[5] = h.x1; o[6] = h.add;
+    }
+  }
+  return PTYCHO_OK;
+}
+
 extern "C" ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t cols, int32_t halo,
                                           const int32_t* tile_owner, const void* nccl_id, int32_t rank,
                                           int32_t nranks) {
   if (!ctx) return PTYCHO_EARG;
   if (ctx->tiles_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles already called");
   const auto& cfg = ctx->cfg;
-  if (rows < 1 || cols < 1 || rows > cfg.height || cols > cfg.width || halo < 0)
+  if (!grid_ok(cfg.height, cfg.width, rows, cols, halo))
     return fail(ctx, PTYCHO_EARG, "bad grid %dx%d halo %d for object %dx%d", rows, cols, halo, cfg.height, cfg.width);
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, PTYCHO_EARG, "bad rank %d / %d", rank, nranks);
   if (nranks > 1 && !nccl_id) return fail(ctx, PTYCHO_EARG, "nccl_id required when nranks > 1");
@@ -227,51 +323,13 @@ extern "C" ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t 
   ctx->halo = halo;
   ctx->rank = rank;
   ctx->nranks = nranks;
-  ctx->tiles.assign(rows * cols, Tile());
-  for (int r = 0; r < rows; ++r)
-    for (int c = 0; c < cols; ++c) {
-      Tile& t = ctx->tiles[r * cols + c];
-      t.k = r * cols + c;
-      t.r = r;
-      t.c = c;
-      split(cfg.height, rows, r, &t.iy0, &t.iy1);
-      split(cfg.width, cols, c, &t.ix0, &t.ix1);
-      t.ey0 = std::max(0, t.iy0 - halo);
-      t.ex0 = std::max(0, t.ix0 - halo);
-      t.ey1 = std::min(cfg.height, t.iy1 + halo);
-      t.ex1 = std::min(cfg.width, t.ix1 + halo);
-      t.eh = t.ey1 - t.ey0;
-      t.ew = t.ex1 - t.ex0;
-      t.pitch0 = (t.ew + 31) / 32 * 32;
-      t.pitch1 = (t.eh + 31) / 32 * 32;
-      const long long a = (long long)t.eh * t.pitch0, b = (long long)t.ew * t.pitch1;
-      t.slice_stride = (std::max(a, b) + 31) / 32 * 32;
-      t.owner = tile_owner ? tile_owner[t.k] : rank;
-      if (t.owner < 0 || t.owner >= nranks) return fail(ctx, PTYCHO_EARG, "tile_owner[%d] = %d", t.k, t.owner);
-      if (t.owner == rank) ctx->local.push_back(t.k);
-    }
-  // APPP hop list in the global order every rank follows (Fig. forward_backward a-d)
-  auto T = [&](int r, int c) -> Tile& { return ctx->tiles[r * cols + c]; };
-  for (int c = 0; c < cols; ++c)
-    for (int r = 0; r + 1 < rows; ++r) {  // vertical forward: ADD down the column
-      Tile &a = T(r, c), &b = T(r + 1, c);
-      ctx->hops.push_back({a.k, b.k, std::max(a.ey0, b.ey0), std::min(a.ey1, b.ey1), a.ex0, a.ex1, 1});
-    }
-  for (int c = 0; c < cols; ++c)
-    for (int r = rows - 1; r >= 1; --r) {  // vertical backward: REPLACE up the column
-      Tile &a = T(r, c), &b = T(r - 1, c);
-      ctx->hops.push_back({a.k, b.k, std::max(a.ey0, b.ey0), std::min(a.ey1, b.ey1), a.ex0, a.ex1, 0});
-    }
-  for (int r = 0; r < rows; ++r)
-    for (int c = 0; c + 1 < cols; ++c) {  // horizontal forward over the full extended height Y_r
-      Tile &a = T(r, c), &b = T(r, c + 1);
-      ctx->hops.push_back({a.k, b.k, a.ey0, a.ey1, std::max(a.ex0, b.ex0), std::min(a.ex1, b.ex1), 1});
-    }
-  for (int r = 0; r < rows; ++r)
-    for (int c = cols - 1; c >= 1; --c) {  // horizontal backward
-      Tile &a = T(r, c), &b = T(r, c - 1);
-      ctx->hops.push_back({a.k, b.k, a.ey0, a.ey1, std::max(a.ex0, b.ex0), std::min(a.ex1, b.ex1), 0});
-    }
+  build_tiles(cfg.height, cfg.width, rows, cols, halo, ctx->tiles);
+  for (Tile& t : ctx->tiles) {
+    t.owner = tile_owner ? tile_owner[t.k] : rank;
+    if (t.owner < 0 || t.owner >= nranks) return fail(ctx, PTYCHO_EARG, "tile_owner[%d] = %d", t.k, t.owner);
+    if (t.owner == rank) ctx->local.push_back(t.k);
+  }
+  build_hops(ctx->tiles, rows, cols, ctx->hops);
   CK(cudaSetDevice(ctx->device));
   for (int k : ctx->local) {
     CK(cudaStreamCreateWithFlags(&ctx->tiles[k].stream, cudaStreamNonBlocking));
@@ -650,6 +708,7 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   a.wtab = ctx->wtab;
   a.htab = ctx->htab;
   a.sigma = ctx->cfg.sigma;
+  a.sigma_pi = (float)((double)ctx->cfg.sigma / M_PI);
   a.alpha = ctx->cfg.alpha;
   a.thr = (float)(ctx->cfg.tau * ctx->probe_norm / ctx->cfg.n);
   return a;

@@ -27,11 +27,12 @@ struct PassArgs {
   int* cursor;              // current local probe index (device)
   unsigned* done;           // block-completion counter for the cursor advance
   double* loss_part;        // per-CTA loss partial sums
-  const float2* wtab;       // W_N^k = exp(-2 pi i k/N), k < N (rounded from double)
+  const float2* wtab;       // wtab[k*Q + q] = W_N^{qk} = exp(-2 pi i qk/N) (rounded from double)
   const float2* htab;       // H_1[u]/N = exp(-i pi c m_u^2/N^2)/N (rounded from double)
   float* gexport;           // debug: gradient out [S][N][N] natural (GRAD passes) or nullptr
   float2* natural_out;      // debug: exit wave out [N][N] natural
   float sigma, alpha, thr;  // t = exp(i sigma V); per-probe step; |Psi| threshold (true scale)
+  float sigma_pi;           // sigma / pi (t = sincospi(sigma_pi V), rounded from double)
   int s;                    // slice index of this pass (TRANSMIT / GRAD)
   int advance;              // last block increments *cursor when done
   int natural_transposed;   // debug store: lines are columns (1) or rows (0)

@@ -92,58 +92,104 @@ template <> struct Geo<64> { static constexpr int P = 8, Q = 8; };
 template <> struct Geo<256> { static constexpr int P = 16, Q = 16; };
 template <> struct Geo<1024> { static constexpr int P = 32, Q = 32; };
 
-// Unnormalised N-point DFT of one line; thread q holds x[q + Q*k] in and X[q + Q*k] out.
-// ex: this line's exchange buffer P x (Q+1) float2.
-template <int N, bool INV>
-__device__ __forceinline__ void line_fft(float2 (&x)[Geo<N>::P], float2* __restrict__ ex, int q,
-                                         const float2* __restrict__ wtab) {
+// Unnormalised forward N-point DFT of one line; thread q holds x[q + Q*k] in and X[q + Q*k]
+// out.  ex: this line's exchange buffer P x (Q+1) float2; tw: shared twiddles tw[k*Q+q] =
+// W_N^{qk}.  Inverse transforms are computed as conj(F(conj(.))) by the callers, so only this
+// one body exists in the SASS of a pass kernel (the pass loop below is not unrolled).
+template <int N>
+__device__ __forceinline__ void fft_fwd(float2 (&x)[Geo<N>::P], float2* __restrict__ ex, int q,
+                                        const float2* __restrict__ tw) {
   constexpr int P = Geo<N>::P, Q = Geo<N>::Q;
-  dft_reg<P, INV>(x);
+  dft_reg<P, false>(x);
 #pragma unroll
-  for (int k = 1; k < P; ++k) {
-    const float2 w = __ldg(wtab + q * k);
-    x[k] = INV ? cmulc(x[k], w) : cmul(x[k], w);
-  }
+  for (int k = 1; k < P; ++k) x[k] = cmul(x[k], tw[k * Q + q]);
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < P; ++k) ex[k * (Q + 1) + q] = x[k];
   __syncwarp();
 #pragma unroll
   for (int n = 0; n < Q; ++n) x[n] = ex[q * (Q + 1) + n];
-  dft_reg<Q, INV>(x);
+  __syncwarp();
+  dft_reg<Q, false>(x);
 }
 
-// 1-D Fresnel propagation along the line: IFFT(H_1/N . FFT(x)) (ADJ: conj(H_1)).
-template <int N, bool ADJ>
-__device__ __forceinline__ void line_prop(float2 (&x)[Geo<N>::P], float2* __restrict__ ex, int q,
-                                          const float2* __restrict__ wtab, const float2* __restrict__ htab) {
-  constexpr int P = Geo<N>::P, Q = Geo<N>::Q;
-  line_fft<N, false>(x, ex, q, wtab);
-#pragma unroll
-  for (int k = 0; k < P; ++k) {
-    const float2 h = __ldg(htab + q + Q * k);
-    x[k] = ADJ ? cmulc(x[k], h) : cmul(x[k], h);
+// ------------------------------------------------------------------------------------------
+// pass kernel
+// ------------------------------------------------------------------------------------------
+// Pointwise steps between forward-DFT calls (F).  With F^-1 = conj o F o conj (unnormalised,
+// 1/N folded into H):
+//   propagation  P  = F^-1 (H/N) F       ->  F ; y <- conj(H/N) conj(y) ; F ; result = conj(z)
+//   adjoint      P^H = F^-1 conj(H)/N F  ->  F ; y <- (H/N) conj(y)      ; F ; result = conj(z)
+// so after the second F of a propagation the register value is the conjugate of the true field
+// ("conj pending"); the next step folds that conjugation in.
+enum Step : int {
+  S_NONE = 0,
+  S_HC_FWD,      // y <- conj(H) conj(y)            (inside P)
+  S_HC_ADJ,      // y <- H conj(y)                  (inside P^H)
+  S_CONJ,        // y <- conj(y)                    (start an inverse transform of a true field)
+  S_TRANSMIT,    // psi = conj(y) [cp] or y ; phi = t_s psi ; stash phi ; y <- phi
+  S_RESID,       // X = y ; loss ; chi = r X/(|X| N) ; y <- conj(chi)   (start of the 2-D inverse)
+  S_SIMUL,       // |X| -> measurement store
+  S_GRAD,        // chi_phi = conj(y) ; g ; AccBuf/V update ; y <- conj(t) chi_phi
+};
+
+// Per pass kind: steps before each F call, the step after the last F, and whether the stored
+// field is "conj pending".
+struct Plan {
+  int nf;          // number of forward DFT calls
+  int pre[4];      // step applied before F call i
+  int post;        // step after the last F
+  bool store_conj; // stored value = conj(register)
+  bool transmit_cp;// S_TRANSMIT input is conj pending
+};
+
+__host__ __device__ constexpr Plan plan_of(int kind) {
+  switch (kind) {
+    case K_FWD_FIRST_PROP: return {2, {S_TRANSMIT, S_HC_FWD, 0, 0}, S_NONE, true, false};
+    case K_FWD_FIRST_FFT: return {1, {S_TRANSMIT, 0, 0, 0}, S_NONE, false, false};
+    case K_FWD_MID: return {4, {S_NONE, S_HC_FWD, S_TRANSMIT, S_HC_FWD}, S_NONE, true, true};
+    case K_FWD_LAST: return {3, {S_NONE, S_HC_FWD, S_TRANSMIT, 0}, S_NONE, false, true};
+    case K_TURN: return {2, {S_NONE, S_RESID, 0, 0}, S_NONE, true, false};
+    case K_SIMULATE: return {1, {S_NONE, 0, 0, 0}, S_SIMUL, false, false};
+    case K_BWD_LAST_PROP: return {3, {S_CONJ, S_GRAD, S_HC_ADJ, 0}, S_NONE, true, false};
+    case K_BWD_LAST_END: return {1, {S_CONJ, 0, 0, 0}, S_GRAD, false, false};
+    case K_BWD_MID: return {4, {S_NONE, S_HC_ADJ, S_GRAD, S_HC_ADJ}, S_NONE, true, false};
+    case K_BWD_END: return {2, {S_NONE, S_HC_ADJ, 0, 0}, S_GRAD, false, false};
+    case K_EXIT_COMPLETE: return {2, {S_NONE, S_HC_FWD, 0, 0}, S_NONE, true, false};
+    default: return {0, {0, 0, 0, 0}, 0, false, false};
   }
-  line_fft<N, true>(x, ex, q, wtab);
 }
 
-enum : int { OP_NONE = 0, OP_PROPF, OP_PROPA, OP_FFT, OP_IFFT };
-enum : int { MID_NONE = 0, MID_TRANSMIT, MID_RESID, MID_SIMUL, MID_GRAD };
-enum : int { ST_NONE = 0, ST_TRANS, ST_NATURAL };
+__host__ __device__ constexpr bool has_step(const Plan& p, int st) {
+  return p.post == st || (p.nf > 0 && p.pre[0] == st) || (p.nf > 1 && p.pre[1] == st) ||
+         (p.nf > 2 && p.pre[2] == st) || (p.nf > 3 && p.pre[3] == st);
+}
 
-template <int N, int OP>
-__device__ __forceinline__ void apply_op(float2 (&x)[Geo<N>::P], float2* ex, int q, const PassArgs& a) {
-  if constexpr (OP == OP_PROPF) line_prop<N, false>(x, ex, q, a.wtab, a.htab);
-  if constexpr (OP == OP_PROPA) line_prop<N, true>(x, ex, q, a.wtab, a.htab);
-  if constexpr (OP == OP_FFT) line_fft<N, false>(x, ex, q, a.wtab);
-  if constexpr (OP == OP_IFFT) line_fft<N, true>(x, ex, q, a.wtab);
+__host__ __device__ constexpr bool kind_transmit(int k) {
+  return k == K_FWD_FIRST_PROP || k == K_FWD_FIRST_FFT || k == K_FWD_MID || k == K_FWD_LAST;
+}
+__host__ __device__ constexpr bool kind_grad(int k) {
+  return k == K_BWD_LAST_PROP || k == K_BWD_LAST_END || k == K_BWD_MID || k == K_BWD_END;
+}
+__host__ __device__ constexpr bool kind_first(int k) { return k == K_FWD_FIRST_PROP || k == K_FWD_FIRST_FFT; }
+__host__ __device__ constexpr int kind_store(int k) {
+  return k == K_SIMULATE || k == K_BWD_LAST_END || k == K_BWD_END ? 0 : (k == K_EXIT_COMPLETE ? 2 : 1);
 }
 
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// Location of this line inside R_k for slice parity ax: row pointer offset and valid range of
-// the position coordinate.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async4(void* sm, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sm)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* sm, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sm)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Location of this line inside R_k for slice parity ax.
 struct LineLoc {
   long long row;  // offset of (line, pos=0) in the slice, valid only if ok
   int pos0;       // tile-local coordinate of window position 0 along the line
@@ -169,120 +215,223 @@ __device__ __forceinline__ LineLoc line_loc(const PassArgs& a, int ax, int line,
   return L;
 }
 
-template <int N, bool PROBE_IN, int PRE, int MID, int POST, int STORE>
-__global__ void __launch_bounds__(LINES_PER_CTA * Geo<N>::Q)
+// Shared-memory carve-up of a pass CTA.
+template <int N, int KIND>
+struct Smem {
+  static constexpr int P = Geo<N>::P, Q = Geo<N>::Q, L = LINES_PER_CTA;
+  static constexpr size_t tw = 0;                                    // N float2 twiddles
+  static constexpr size_t ht = tw + N * 8;                           // H_1/N, m = 0..N/2 (even in m)
+  static constexpr size_t lines = ht + (N / 2 + 2) * 8;
+  static constexpr size_t ex_b = (size_t)P * (Q + 1) * 8;            // per line
+  static constexpr size_t st_b = kind_grad(KIND) ? (size_t)N * 8 : 0;  // stash prefetch per line
+  static constexpr size_t v_b = (kind_transmit(KIND) || kind_grad(KIND) || KIND == K_TURN) ? (size_t)N * 4 : 0;
+  static constexpr size_t acc_b = kind_grad(KIND) ? (size_t)N * 4 : 0;  // AccBuf prefetch per line
+  static constexpr size_t per_line = ex_b + st_b + v_b + acc_b;
+  static constexpr size_t stage_b = (size_t)N * (L + 1) * 8;         // transposed-store staging
+  static constexpr size_t total = lines + (per_line * L > stage_b ? per_line * L : stage_b);
+};
+
+template <int N, int KIND>
+__global__ void __launch_bounds__(LINES_PER_CTA * Geo<N>::Q, 2)
 pass_kernel(const PassArgs a) {
   constexpr int P = Geo<N>::P, Q = Geo<N>::Q, L = LINES_PER_CTA;
-  extern __shared__ float2 smem[];
-  griddep_wait();
-  griddep_launch();
-
+  constexpr Plan PL = plan_of(KIND);
+  using SM = Smem<N, KIND>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float2* tw = (float2*)(smem + SM::tw);
+  float2* ht = (float2*)(smem + SM::ht);
   const int lw = threadIdx.x / Q, q = threadIdx.x % Q;
   const int line = blockIdx.x * L + lw;
-  const int i = *a.cursor;
+  unsigned char* lbase = smem + SM::lines + lw * SM::per_line;
+  float2* ex = (float2*)lbase;
+  float2* pst = (float2*)(lbase + SM::ex_b);                // prefetched stash row (GRAD)
+  float* pv = (float*)(lbase + SM::ex_b + SM::st_b);        // prefetched V row / amplitude row
+  float* pacc = (float*)(lbase + SM::ex_b + SM::st_b + SM::v_b);  // prefetched AccBuf row (GRAD)
+
+  // ---- before the grid dependency: tables, and prefetches of data written >= 2 kernels ago
+  for (int e = threadIdx.x; e < N; e += L * Q) tw[e] = __ldg(a.wtab + e);
+  for (int e = threadIdx.x; e <= N / 2; e += L * Q) ht[e] = __ldg(a.htab + e);
+  constexpr bool FIRST = kind_first(KIND);
+  int i = 0;
+  if constexpr (!FIRST) i = *a.cursor;
+  if constexpr (FIRST) {
+    griddep_wait();
+    griddep_launch();
+    i = *a.cursor;
+  }
   const int2 ctr = a.centers[i];
   const int wy0 = ctr.x - N / 2, wx0 = ctr.y - N / 2;
-  float2* ex = smem + lw * P * (Q + 1);
-
+  const int ax = a.s & 1;
+  LineLoc LL = line_loc(a, ax, line, wy0, wx0);
+  if constexpr (kind_transmit(KIND) || kind_grad(KIND)) {
+    const long long so = (long long)a.s * a.slice_stride + LL.row;
+    const float* vrow = a.V + so;
+    const float* arow = a.acc + so;
+#pragma unroll 4
+    for (int k = 0; k < P; ++k) {
+      const int j = q + Q * k, p = LL.pos0 + j;
+      if (LL.ok && (unsigned)p < (unsigned)LL.plim) {
+        cp_async4(pv + j, vrow + p);
+        if constexpr (kind_grad(KIND)) cp_async4(pacc + j, arow + p);
+      } else {
+        pv[j] = 0.f;
+        if constexpr (kind_grad(KIND)) pacc[j] = 0.f;
+      }
+    }
+  }
+  if constexpr (kind_grad(KIND)) {
+    const float4* src = (const float4*)(a.stash + (size_t)a.s * N * N + (size_t)line * N);
+    float4* dst = (float4*)pst;
+#pragma unroll 4
+    for (int c = q; c < N / 2; c += Q) cp_async16(dst + c, src + c);
+  }
+  if constexpr (KIND == K_TURN) {
+    const float4* src = (const float4*)(a.amp + (size_t)i * N * N + (size_t)line * N);
+    float4* dst = (float4*)pv;
+#pragma unroll 4
+    for (int c = q; c < N / 4; c += Q) cp_async16(dst + c, src + c);
+  }
+  cp_async_commit();
   float2 x[P];
-  {
-    const float2* src = (PROBE_IN ? a.probe : a.in) + (size_t)line * N + q;
+  if constexpr (FIRST) {
+    const float2* src = a.probe + (size_t)line * N + q;
+#pragma unroll
+    for (int k = 0; k < P; ++k) x[k] = src[Q * k];
+  } else {
+    griddep_wait();
+    griddep_launch();
+    const float2* src = a.in + (size_t)line * N + q;
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = src[Q * k];
   }
+  __syncthreads();  // tables visible
 
-  apply_op<N, PRE>(x, ex, q, a);
-
-  if constexpr (MID == MID_TRANSMIT) {
-    // phi_s = exp(i sigma V_s[win ^ R_k]) psi_s  (t = 1 outside R_k, reading #12); stash phi_s.
-    const int ax = a.s & 1;
-    const LineLoc LL = line_loc(a, ax, line, wy0, wx0);
-    const float* vrow = a.V + (long long)a.s * a.slice_stride + LL.row;
-    float2* st = a.stash + (size_t)a.s * N * N + (size_t)line * N + q;
+  float part = 0.f;  // loss partial (RESID)
+  auto step = [&](int st) {
+    if ((has_step(PL, S_HC_FWD) && st == S_HC_FWD) || (has_step(PL, S_HC_ADJ) && st == S_HC_ADJ)) {
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int p = LL.pos0 + q + Q * k;
-      const float v = (LL.ok && (unsigned)p < (unsigned)LL.plim) ? vrow[p] : 0.f;
-      float sn, cs;
-      sincosf(a.sigma * v, &sn, &cs);
-      x[k] = cmul(x[k], make_float2(cs, sn));
-      st[Q * k] = x[k];
-    }
-  }
-
-  if constexpr (MID == MID_RESID || MID == MID_SIMUL) {
-    // X = raw 2-D DFT (N x true F phi_{S-1}); |Psi| = |X|/N (App. A: |H| = 1).
-    const float invn = 1.0f / (float)N;
-    float* am = a.amp + (size_t)i * N * N + (size_t)line * N + q;
-    float part = 0.f;
+      for (int k = 0; k < P; ++k) {
+        // H_1 depends on m_u^2 only: u = q+Qk for k < P/2, else N-u = Q(P-k) - q (P == Q)
+        const float2 h = ht[k < P / 2 ? q + Q * k : Q * (P - k) - q];
+        const float2 y = x[k];
+        // conj(H) conj(y) = conj(H y) ;  H conj(y)
+        if (st == S_HC_FWD) x[k] = make_float2(h.x * y.x - h.y * y.y, -(h.x * y.y + h.y * y.x));
+        else x[k] = make_float2(h.x * y.x + h.y * y.y, h.y * y.x - h.x * y.y);
+      }
+    } else if (has_step(PL, S_CONJ) && st == S_CONJ) {
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const float m = sqrtf(x[k].x * x[k].x + x[k].y * x[k].y);
-      const float mag = m * invn;
-      if constexpr (MID == MID_SIMUL) {
-        am[Q * k] = mag;
-      } else {
-        const float r = mag - am[Q * k];
+      for (int k = 0; k < P; ++k) x[k].y = -x[k].y;
+    } else if (has_step(PL, S_TRANSMIT) && st == S_TRANSMIT) {
+      // phi_s = exp(i sigma V_s[win ^ R_k]) psi_s  (t = 1 outside R_k, reading #12); stash phi_s
+      cp_async_wait_all();
+      float2* stp = a.stash + (size_t)a.s * N * N + (size_t)line * N + q;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const float v = pv[q + Q * k];
+        float sn, cs;
+        sincospif(a.sigma_pi * v, &sn, &cs);  // exp(i sigma v): exact reduction, no slow path
+        float2 y = x[k];
+        if (PL.transmit_cp) y.y = -y.y;
+        x[k] = cmul(y, make_float2(cs, sn));
+        stp[Q * k] = x[k];
+      }
+    } else if (has_step(PL, S_RESID) && st == S_RESID) {
+      // X = raw 2-D DFT (N x true F phi_{S-1}); |Psi| = |X|/N (App. A: |H| = 1)
+      cp_async_wait_all();
+      __syncwarp();
+      const float invn = 1.0f / (float)N;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const float m = sqrtf(x[k].x * x[k].x + x[k].y * x[k].y);
+        const float mag = m * invn;
+        const float r = mag - pv[q + Q * k];
         part += r * r;
-        // chi_Psi = r Psi/|Psi| (0 where |Psi| <= thr, reading #30), times 1/N for the two
-        // unnormalised inverse line transforms that complete the unitary 2-D inverse.
+        // chi_Psi = r Psi/|Psi| (0 where |Psi| <= thr, reading #30), /N for the two unnormalised
+        // inverse line transforms; conjugated to start the inverse as conj o F o conj.
         const float sc = (mag > a.thr) ? r * invn / m : 0.f;
-        x[k] = make_float2(x[k].x * sc, x[k].y * sc);
+        x[k] = make_float2(x[k].x * sc, -x[k].y * sc);
+      }
+    } else if (has_step(PL, S_SIMUL) && st == S_SIMUL) {
+      const float invn = 1.0f / (float)N;
+      float* am = a.amp + (size_t)i * N * N + (size_t)line * N + q;
+#pragma unroll
+      for (int k = 0; k < P; ++k) am[Q * k] = sqrtf(x[k].x * x[k].x + x[k].y * x[k].y) * invn;
+    } else if (has_step(PL, S_GRAD) && st == S_GRAD) {
+      // chi_phi = conj(y).  g_s = 2 sigma Im(chi conj(phi_s)) (App. A); on win ^ R_k:
+      // AccBuf += g (Alg. 1 step 7), V -= alpha g (step 8); chi <- conj(t_s) chi with t_s from
+      // the PRE-update V.
+      const long long so = (long long)a.s * a.slice_stride + LL.row;
+      float* vrow = a.V + so;
+      float* arow = a.acc + so;
+      cp_async_wait_all();
+      __syncwarp();
+      const float two_sigma = 2.0f * a.sigma;
+      const bool exporting = a.gexport != nullptr;  // debug: write g instead of updating
+      float* vbase = vrow + LL.pos0 + q;
+      float* abase = arow + LL.pos0 + q;
+      const int lim = LL.ok ? LL.plim - LL.pos0 - q : 0;  // element k valid iff 0 <= Qk + pos0 + q < plim
+      const int low = -(LL.pos0 + q);
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        if ((k & 7) == 0) asm volatile("" ::: "memory");
+        const int j = q + Q * k;
+        const float2 ph = pst[j];
+        const float2 chi = make_float2(x[k].x, -x[k].y);
+        const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
+        const float v = pv[j];
+        if (!exporting && Q * k >= low && Q * k < lim) {
+          abase[Q * k] = pacc[j] + g;
+          vbase[Q * k] = v - a.alpha * g;
+        }
+        pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
+        float sn, cs;
+        sincospif(a.sigma_pi * v, &sn, &cs);
+        x[k] = cmulc(chi, make_float2(cs, sn));
+      }
+      if (exporting) {
+        float* o = a.gexport + (size_t)a.s * N * N;
+#pragma unroll 4
+        for (int k = 0; k < P; ++k) {
+          const int j = q + Q * k;
+          o[ax == 0 ? (size_t)line * N + j : (size_t)j * N + line] = pacc[j];
+        }
       }
     }
-    if constexpr (MID == MID_RESID) {
+  };
+
+#pragma unroll 1
+  for (int f = 0; f < PL.nf; ++f) {
+    int st = PL.pre[0];
+    if (f == 1) st = PL.pre[1];
+    if (f == 2) st = PL.pre[2];
+    if (f == 3) st = PL.pre[3];
+    step(st);
+    fft_fwd<N>(x, ex, q, tw);
+  }
+  step(PL.post);
+
+  if constexpr (KIND == K_TURN) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      __shared__ float red[LINES_PER_CTA * Q / 32 + 1];
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double tot = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += (double)red[w];
-        a.loss_part[blockIdx.x] += tot;
-      }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    __shared__ float red[LINES_PER_CTA * Q / 32 + 1];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += (double)red[w];
+      a.loss_part[blockIdx.x] += tot;
     }
   }
 
-  if constexpr (MID == MID_GRAD) {
-    // chi holds chi_phi_s.  g_s = 2 sigma Im(chi conj(phi_s)) (App. A);  on win ^ R_k:
-    // AccBuf += g (Alg. 1 step 7), V -= alpha g (step 8); then chi <- conj(t_s) chi with t_s
-    // from the PRE-update V.
-    const int ax = a.s & 1;
-    const LineLoc LL = line_loc(a, ax, line, wy0, wx0);
-    const long long so = (long long)a.s * a.slice_stride + LL.row;
-    float* vrow = a.V + so;
-    float* arow = a.acc + so;
-    const float2* st = a.stash + (size_t)a.s * N * N + (size_t)line * N + q;
-    const float two_sigma = 2.0f * a.sigma;
+  if constexpr (PL.store_conj) {
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int j = q + Q * k;
-      const int p = LL.pos0 + j;
-      const bool ok = LL.ok && (unsigned)p < (unsigned)LL.plim;
-      const float2 ph = st[Q * k];
-      const float g = two_sigma * (x[k].y * ph.x - x[k].x * ph.y);
-      float v = 0.f;
-      if (ok) v = vrow[p];
-      if (a.gexport != nullptr) {
-        const size_t o = (size_t)a.s * N * N + (ax == 0 ? (size_t)line * N + j : (size_t)j * N + line);
-        a.gexport[o] = g;
-      } else if (ok) {
-        arow[p] += g;
-        vrow[p] = v - a.alpha * g;
-      }
-      float sn, cs;
-      sincosf(a.sigma * v, &sn, &cs);
-      x[k] = cmulc(x[k], make_float2(cs, sn));
-    }
+    for (int k = 0; k < P; ++k) x[k].y = -x[k].y;
   }
-
-  apply_op<N, POST>(x, ex, q, a);
-
-  if constexpr (STORE == ST_TRANS) {
+  constexpr int STORE = kind_store(KIND);
+  if constexpr (STORE == 1) {
     // out[j][line]: stage the CTA's L lines, then write L consecutive complex per output row.
     __syncthreads();
-    float2* stg = smem;
+    float2* stg = (float2*)(smem + SM::lines);
 #pragma unroll
     for (int k = 0; k < P; ++k) stg[(q + Q * k) * (L + 1) + lw] = x[k];
     __syncthreads();
@@ -293,7 +442,7 @@ pass_kernel(const PassArgs a) {
       dst[(size_t)j * N + l] = stg[j * (L + 1) + l];
     }
   }
-  if constexpr (STORE == ST_NATURAL) {
+  if constexpr (STORE == 2) {
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       const int j = q + Q * k;
@@ -316,18 +465,10 @@ pass_kernel(const PassArgs a) {
   }
 }
 
-template <int N>
-static size_t pass_smem() {
-  constexpr int P = Geo<N>::P, Q = Geo<N>::Q, L = LINES_PER_CTA;
-  const size_t ex = (size_t)L * P * (Q + 1) * sizeof(float2);
-  const size_t st = (size_t)N * (L + 1) * sizeof(float2);
-  return ex > st ? ex : st;
-}
-
-template <int N, bool PROBE_IN, int PRE, int MID, int POST, int STORE>
+template <int N, int KIND>
 static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) {
-  auto kern = pass_kernel<N, PROBE_IN, PRE, MID, POST, STORE>;
-  const size_t smem = pass_smem<N>();
+  auto kern = pass_kernel<N, KIND>;
+  const size_t smem = Smem<N, KIND>::total;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -350,17 +491,17 @@ static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) 
 template <int N>
 static cudaError_t launch_pass_n(PassKind kind, const PassArgs& a, cudaStream_t s, bool pdl) {
   switch (kind) {
-    case K_FWD_FIRST_PROP: return launch_one<N, true, OP_NONE, MID_TRANSMIT, OP_PROPF, ST_TRANS>(a, s, pdl);
-    case K_FWD_FIRST_FFT: return launch_one<N, true, OP_NONE, MID_TRANSMIT, OP_FFT, ST_TRANS>(a, s, pdl);
-    case K_FWD_MID: return launch_one<N, false, OP_PROPF, MID_TRANSMIT, OP_PROPF, ST_TRANS>(a, s, pdl);
-    case K_FWD_LAST: return launch_one<N, false, OP_PROPF, MID_TRANSMIT, OP_FFT, ST_TRANS>(a, s, pdl);
-    case K_TURN: return launch_one<N, false, OP_FFT, MID_RESID, OP_IFFT, ST_TRANS>(a, s, pdl);
-    case K_SIMULATE: return launch_one<N, false, OP_FFT, MID_SIMUL, OP_NONE, ST_NONE>(a, s, pdl);
-    case K_BWD_LAST_PROP: return launch_one<N, false, OP_IFFT, MID_GRAD, OP_PROPA, ST_TRANS>(a, s, pdl);
-    case K_BWD_LAST_END: return launch_one<N, false, OP_IFFT, MID_GRAD, OP_NONE, ST_NONE>(a, s, pdl);
-    case K_BWD_MID: return launch_one<N, false, OP_PROPA, MID_GRAD, OP_PROPA, ST_TRANS>(a, s, pdl);
-    case K_BWD_END: return launch_one<N, false, OP_PROPA, MID_GRAD, OP_NONE, ST_NONE>(a, s, pdl);
-    case K_EXIT_COMPLETE: return launch_one<N, false, OP_PROPF, MID_NONE, OP_NONE, ST_NATURAL>(a, s, pdl);
+    case K_FWD_FIRST_PROP: return launch_one<N, K_FWD_FIRST_PROP>(a, s, pdl);
+    case K_FWD_FIRST_FFT: return launch_one<N, K_FWD_FIRST_FFT>(a, s, pdl);
+    case K_FWD_MID: return launch_one<N, K_FWD_MID>(a, s, pdl);
+    case K_FWD_LAST: return launch_one<N, K_FWD_LAST>(a, s, pdl);
+    case K_TURN: return launch_one<N, K_TURN>(a, s, pdl);
+    case K_SIMULATE: return launch_one<N, K_SIMULATE>(a, s, pdl);
+    case K_BWD_LAST_PROP: return launch_one<N, K_BWD_LAST_PROP>(a, s, pdl);
+    case K_BWD_LAST_END: return launch_one<N, K_BWD_LAST_END>(a, s, pdl);
+    case K_BWD_MID: return launch_one<N, K_BWD_MID>(a, s, pdl);
+    case K_BWD_END: return launch_one<N, K_BWD_END>(a, s, pdl);
+    case K_EXIT_COMPLETE: return launch_one<N, K_EXIT_COMPLETE>(a, s, pdl);
     default: return cudaErrorInvalidValue;
   }
 }

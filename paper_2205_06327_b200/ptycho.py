@@ -43,6 +43,9 @@ _SIGS = {
     "ptycho_nccl_unique_id": [_P, _c.c_size_t],
     "ptycho_set_tiles": [_P, _c.c_int32, _c.c_int32, _c.c_int32, _P, _P, _c.c_int32, _c.c_int32],
     "ptycho_set_scan": [_P, _P, _c.c_int64],
+    "ptycho_tile_geometry": [_c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _P],
+    "ptycho_appp_schedule": [_c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _P, _c.c_int32,
+                             _c.POINTER(_c.c_int32)],
     "ptycho_local_probes": [_P, _P, _c.POINTER(_c.c_int64)],
     "ptycho_tile_probe_count": [_P, _c.c_int32, _c.POINTER(_c.c_int64)],
     "ptycho_tile_rect": [_P, _c.c_int32, _P, _P],
@@ -76,6 +79,28 @@ lib.ptycho_last_error.restype = _c.c_char_p
 ptycho_last_error = lib.ptycho_last_error
 
 EXPORTED = sorted(list(_SIGS) + ["ptycho_last_error"])
+
+
+def tile_geometry(height, width, rows, cols, halo):
+    """[(ext, interior)] per tile from the library's host geometry (no GPU needed)."""
+    out = np.zeros((rows * cols, 8), np.int32)
+    st = lib.ptycho_tile_geometry(height, width, rows, cols, halo, out.ctypes.data)
+    if st != 0:
+        raise PtychoError(st, lib.ptycho_last_error(None).decode())
+    return [(tuple(int(v) for v in r[:4]), tuple(int(v) for v in r[4:])) for r in out]
+
+
+def appp_schedule(height, width, rows, cols, halo):
+    """The library's APPP hop list (src, dst, y0, y1, x0, x1, add), global order (no GPU needed)."""
+    cnt = ctypes.c_int32()
+    st = lib.ptycho_appp_schedule(height, width, rows, cols, halo, None, 0, ctypes.byref(cnt))
+    if st != 0:
+        raise PtychoError(st, lib.ptycho_last_error(None).decode())
+    out = np.zeros((cnt.value, 7), np.int32)
+    st = lib.ptycho_appp_schedule(height, width, rows, cols, halo, out.ctypes.data, cnt.value, ctypes.byref(cnt))
+    if st != 0:
+        raise PtychoError(st, lib.ptycho_last_error(None).decode())
+    return [tuple(int(v) for v in r) for r in out]
 
 
 class PtychoError(RuntimeError):
