@@ -43,7 +43,7 @@ struct Tile {
   float2* wf[2] = {nullptr, nullptr};
   float* amp = nullptr;
   int2* centers = nullptr;
-  int* cursor = nullptr;
+  int4* desc = nullptr;
   unsigned* done = nullptr;
   double* loss_part = nullptr;
   cudaStream_t stream = nullptr;
@@ -131,7 +131,6 @@ static int slices_odd(int S) { return S / 2; }
 // ------------------------------------------------------------------------------------------
 // tiny device helpers launched from here
 // ------------------------------------------------------------------------------------------
-__global__ void set_int_kernel(int* p, int v) { *p = v; }
 
 // ------------------------------------------------------------------------------------------
 // lifecycle
@@ -163,14 +162,9 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   }
   // tables in double, rounded to float: W_N^k and H_1[u]/N (reading #3, #4)
   const int n = cfg->n;
-  ctx->h_wtab.resize(n);
+  ctx->h_wtab.resize(twiddle_table_size(n));
+  fill_twiddles(n, ctx->h_wtab.data());
   ctx->h_htab.resize(n);
-  const int Q = (int)std::lround(std::sqrt((double)n));  // N = P*Q with P = Q (kernels.cu Geo<N>)
-  for (int k = 0; k < n / Q; ++k)
-    for (int q = 0; q < Q; ++q) {  // four-step twiddle W_N^{qk}, stored [k][q] (coalesced per line)
-      const double th = -2.0 * M_PI * (double)(q * k) / (double)n;
-      ctx->h_wtab[k * Q + q] = make_float2((float)std::cos(th), (float)std::sin(th));
-    }
   for (int k = 0; k < n; ++k) {
     const double m = (k < n / 2) ? (double)k : (double)(k - n);
     const double ph = -M_PI * (double)cfg->prop_c * m * m / ((double)n * (double)n);
@@ -421,7 +415,7 @@ static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
     off = align_up(off + bytes);
     return p;
   };
-  ctx->wtab = (float2*)take(n * sizeof(float2));
+  ctx->wtab = (float2*)take(ctx->h_wtab.size() * sizeof(float2));
   ctx->htab = (float2*)take(n * sizeof(float2));
   ctx->probe = (float2*)take(n2 * sizeof(float2));
   ctx->dscratch = (double*)take(64 * sizeof(double));
@@ -452,7 +446,7 @@ static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
     t.wf[1] = (float2*)take(n2 * sizeof(float2));
     t.amp = (float*)take(std::max<size_t>(t.probes.size(), 1) * n2 * sizeof(float));
     t.centers = (int2*)take(std::max<size_t>(t.probes.size(), 1) * sizeof(int2));
-    t.cursor = (int*)take(sizeof(int));
+    t.desc = (int4*)take(sizeof(int4));
     t.done = (unsigned*)take(sizeof(unsigned));
     t.loss_part = (double*)take((n / LINES_PER_CTA) * sizeof(double));
   }
@@ -488,7 +482,8 @@ extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_de
   ctx->ws_bytes = bytes;
   plan_workspace(ctx, true);
   const size_t n = ctx->cfg.n;
-  CK(cudaMemcpyAsync(ctx->wtab, ctx->h_wtab.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->wtab, ctx->h_wtab.data(), ctx->h_wtab.size() * sizeof(float2), cudaMemcpyHostToDevice,
+                     ctx->stream));
   CK(cudaMemcpyAsync(ctx->htab, ctx->h_htab.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
   for (int k : ctx->local) {
     Tile& t = ctx->tiles[k];
@@ -496,7 +491,7 @@ extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_de
     for (size_t j = 0; j < t.probes.size(); ++j)
       hc[j] = make_int2(ctx->centers[2 * t.probes[j]], ctx->centers[2 * t.probes[j] + 1]);
     CK(cudaMemcpyAsync(t.centers, hc.data(), hc.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemsetAsync(t.cursor, 0, sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(t.desc, 0, sizeof(int4), ctx->stream));
     CK(cudaMemsetAsync(t.done, 0, sizeof(unsigned), ctx->stream));
     CK(cudaMemsetAsync(t.loss_part, 0, (n / LINES_PER_CTA) * sizeof(double), ctx->stream));
     CK(cudaMemsetAsync(t.amp, 0, std::max<size_t>(t.probes.size(), 1) * n * n * sizeof(float), ctx->stream));
@@ -702,7 +697,8 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   a.probe = ctx->probe;
   a.amp = t.amp;
   a.centers = t.centers;
-  a.cursor = t.cursor;
+  a.desc = t.desc;
+  a.n_probes = (int)t.probes.size();
   a.done = t.done;
   a.loss_part = t.loss_part;
   a.wtab = ctx->wtab;
@@ -792,9 +788,8 @@ static ptycho_status ensure_graph(ptycho_ctx ctx, Tile& t) {
 }
 
 static ptycho_status set_cursor(ptycho_ctx ctx, Tile& t, int v, cudaStream_t st) {
-  set_int_kernel<<<1, 1, 0, st>>>(t.cursor, v);
+  CK(launch_set_desc(t.desc, t.centers, v, (int)t.probes.size(), ctx->cfg.n, st));
   ++ctx->launches;
-  CK(cudaGetLastError());
   return PTYCHO_OK;
 }
 

@@ -11,7 +11,7 @@ namespace ptycho {
 constexpr int LINES_PER_CTA = 4;
 
 // Everything a pass kernel needs; passed by value (baked into the per-probe CUDA graph, the
-// probe index itself is read from *cursor on the device).
+// probe itself is read from *desc on the device).
 struct PassArgs {
   float* V;                 // V_k, slice s at V + s*slice_stride; layout L_{s&1}
   float* acc;               // AccBuf_k, same layout as V
@@ -24,17 +24,18 @@ struct PassArgs {
   const float2* probe;      // p, [N][N] natural
   float* amp;               // measurement store [n_k][N][N], layout L_{S&1}, DC at [0][0]
   const int2* centers;      // (cy, cx) of the tile's probes, local order
-  int* cursor;              // current local probe index (device)
+  int4* desc;               // current probe {local index, window y0, window x0, 0} (device)
   unsigned* done;           // block-completion counter for the cursor advance
   double* loss_part;        // per-CTA loss partial sums
-  const float2* wtab;       // wtab[k*Q + q] = W_N^{qk} = exp(-2 pi i qk/N) (rounded from double)
+  const float2* wtab;       // engine twiddle table (fill_twiddles; rounded from double)
   const float2* htab;       // H_1[u]/N = exp(-i pi c m_u^2/N^2)/N (rounded from double)
   float* gexport;           // debug: gradient out [S][N][N] natural (GRAD passes) or nullptr
   float2* natural_out;      // debug: exit wave out [N][N] natural
   float sigma, alpha, thr;  // t = exp(i sigma V); per-probe step; |Psi| threshold (true scale)
   float sigma_pi;           // sigma / pi (t = sincospi(sigma_pi V), rounded from double)
   int s;                    // slice index of this pass (TRANSMIT / GRAD)
-  int advance;              // last block increments *cursor when done
+  int advance;              // last block advances *desc to the next probe when done
+  int n_probes;             // probes of this tile (desc stops at the last one)
   int natural_transposed;   // debug store: lines are columns (1) or rows (0)
 };
 
@@ -68,6 +69,11 @@ cudaError_t launch_acc_step(float* V, float* acc, long long n, float alpha, cuda
 // measurement store: dst[c][.][.] from src[c][N][N] with ifftshift / sqrt / transpose options
 cudaError_t launch_amp_load(float* dst, const float* src, int count, int n, int shift, int intensity,
                             int transpose, cudaStream_t stream);
+// twiddle table of the FFT engine for window n (layout private to kernels.cu)
+size_t twiddle_table_size(int n);
+void fill_twiddles(int n, float2* tw);
+// *desc = probe v of the tile (v clamped to [0, nk))
+cudaError_t launch_set_desc(int4* desc, const int2* centers, int v, int nk, int n, cudaStream_t stream);
 cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t stream);
 cudaError_t launch_sum_double(const double* parts, int n, double* out, cudaStream_t stream);
 

@@ -58,59 +58,240 @@ __device__ __forceinline__ float2 twmul32(float2 a, int m) {
   return make_float2(a.x * c + a.y * s, a.y * c - a.x * s);
 }
 
-// In-register DFT of size P (<= 32), natural order in and out (radix-2 DIT on a compile-time
-// bit-reversed register permutation).  Forward: exp(-2 pi i jk/P), unnormalised.
-template <int P, bool INV>
-__device__ __forceinline__ void dft_reg(float2 (&x)[P]) {
-  constexpr int LOG = Log2<P>::v;
+// In-register forward DFT of size P in {2,4,8,16,32}, natural order in and out, unnormalised
+// (exp(-2 pi i jk/P)).  Mixed radix: P = A*B with A = 4 (A = 2 for P = 2, 8): B-point DFTs on
+// the A decimated subsequences, twiddles W_P^{n1 k2} (compile-time, rounded from double; the
+// trivial ones are exact sign/swaps), then A-point DFTs.  All indices are compile-time, so the
+// sub-arrays are register renames.
+__device__ __forceinline__ void dft2(float2& a, float2& b) {
+  const float2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+__device__ __forceinline__ void dft4(float2& a, float2& b, float2& c, float2& d) {
+  const float2 t0 = cadd(a, c), t1 = csub(a, c), t2 = cadd(b, d), t3 = csub(b, d);
+  a = cadd(t0, t2);
+  c = csub(t0, t2);
+  b = make_float2(t1.x + t3.y, t1.y - t3.x);  // t1 - i t3
+  d = make_float2(t1.x - t3.y, t1.y + t3.x);  // t1 + i t3
+}
+
+template <int P> struct DftReg {
+  static constexpr int A = (P == 8) ? 2 : 4, B = P / A;
+  __device__ __forceinline__ static void run(float2 (&x)[P]) {
+    float2 y[A][B];
 #pragma unroll
-  for (int i = 0; i < P; ++i) {
-    const int j = brev(i, LOG);
-    if (j > i) {
-      const float2 t = x[i];
-      x[i] = x[j];
-      x[j] = t;
+    for (int n1 = 0; n1 < A; ++n1) {
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) y[n1][n2] = x[n1 + A * n2];
+      DftReg<B>::run(y[n1]);
+#pragma unroll
+      for (int k2 = 1; k2 < B; ++k2) y[n1][k2] = twmul32<false>(y[n1][k2], n1 * k2 * (32 / P));
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) {
+      float2 z[A];
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) z[n1] = y[n1][k2];
+      DftReg<A>::run(z);
+#pragma unroll
+      for (int k1 = 0; k1 < A; ++k1) x[k2 + B * k1] = z[k1];
     }
   }
-#pragma unroll
-  for (int half = 1; half < P; half <<= 1) {
-#pragma unroll
-    for (int i = 0; i < P; i += 2 * half) {
-#pragma unroll
-      for (int k = 0; k < half; ++k) {
-        const float2 b = twmul32<INV>(x[i + k + half], k * (32 / (2 * half)));
-        const float2 a = x[i + k];
-        x[i + k] = cadd(a, b);
-        x[i + k + half] = csub(a, b);
-      }
-    }
+};
+template <> struct DftReg<2> {
+  __device__ __forceinline__ static void run(float2 (&x)[2]) { dft2(x[0], x[1]); }
+};
+template <> struct DftReg<4> {
+  __device__ __forceinline__ static void run(float2 (&x)[4]) { dft4(x[0], x[1], x[2], x[3]); }
+};
+
+// exp(i x) for the transmission t = exp(i sigma V): Cephes minimax polynomials on |x| <= pi/4
+// (about 1 ulp, no range reduction -- sigma V is a small phase for any physical potential),
+// sincospi with its exact reduction otherwise.
+__device__ __forceinline__ void sincos_t(float x, float* sn, float* cs) {
+  if (fabsf(x) <= 0.785398163f) {
+    const float z = x * x;
+    *sn = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * x, x);
+    *cs = fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f), z * z,
+               fmaf(-0.5f, z, 1.0f));
+  } else {
+    sincospif(x * 0.318309886183790672f, sn, cs);
   }
 }
 
-template <int N> struct Geo;
-template <> struct Geo<64> { static constexpr int P = 8, Q = 8; };
-template <> struct Geo<256> { static constexpr int P = 16, Q = 16; };
-template <> struct Geo<1024> { static constexpr int P = 32, Q = 32; };
+// ------------------------------------------------------------------------------------------
+// FFT engines.  A line of N complex values is held by T threads, E = N/T elements each.
+// Distribution D0 (natural): thread t holds element t + T*k in register k.  dit() computes the
+// unnormalised forward DFT taking D0 to an engine-specific distribution D1; dif() computes the
+// same DFT taking D1 to D0.  idx(dist, t, k) = natural index of register k.  The pass kernel
+// alternates dit, dif, dit, dif, so FFT -> pointwise -> FFT never needs a reordering pass.
+// ------------------------------------------------------------------------------------------
 
-// Unnormalised forward N-point DFT of one line; thread q holds x[q + Q*k] in and X[q + Q*k]
-// out.  ex: this line's exchange buffer P x (Q+1) float2; tw: shared twiddles tw[k*Q+q] =
-// W_N^{qk}.  Inverse transforms are computed as conj(F(conj(.))) by the callers, so only this
-// one body exists in the SASS of a pass kernel (the pass loop below is not unrolled).
-template <int N>
-__device__ __forceinline__ void fft_fwd(float2 (&x)[Geo<N>::P], float2* __restrict__ ex, int q,
-                                        const float2* __restrict__ tw) {
-  constexpr int P = Geo<N>::P, Q = Geo<N>::Q;
-  dft_reg<P, false>(x);
+// Four-step P x P (N = 64, 256): T = P threads, D1 == D0; tw[k*P + q] = W_N^{qk}.
+template <int P>
+struct EngFour {
+  static constexpr int N = P * P, T = P, E = P;
+  static constexpr int EX = P * (P + 1);  // exchange buffer per line (float2)
+  static constexpr int TW = N;            // twiddle table (float2)
+  __device__ __forceinline__ static int idx(int, int t, int k) { return t + T * k; }
+  __device__ __forceinline__ static void sync_line(int) { __syncwarp(); }
+  __device__ __forceinline__ static void fft(float2 (&x)[E], float2* __restrict__ ex, int q,
+                                            const float2* __restrict__ tw) {
+    DftReg<P>::run(x);
 #pragma unroll
-  for (int k = 1; k < P; ++k) x[k] = cmul(x[k], tw[k * Q + q]);
-  __syncwarp();
+    for (int k = 1; k < P; ++k) x[k] = cmul(x[k], tw[k * P + q]);
+    __syncwarp();
 #pragma unroll
-  for (int k = 0; k < P; ++k) ex[k * (Q + 1) + q] = x[k];
-  __syncwarp();
+    for (int k = 0; k < P; ++k) ex[k * (P + 1) + q] = x[k];
+    __syncwarp();
 #pragma unroll
-  for (int n = 0; n < Q; ++n) x[n] = ex[q * (Q + 1) + n];
-  __syncwarp();
-  dft_reg<Q, false>(x);
+    for (int n = 0; n < P; ++n) x[n] = ex[q * (P + 1) + n];
+    __syncwarp();
+    DftReg<P>::run(x);
+  }
+  __device__ __forceinline__ static void dit(float2 (&x)[E], float2* ex, int t, const float2* tw, int) {
+    fft(x, ex, t, tw);
+  }
+  __device__ __forceinline__ static void dif(float2 (&x)[E], float2* ex, int t, const float2* tw, int) {
+    fft(x, ex, t, tw);
+  }
+  static void fill(float2* tw) {
+    for (int k = 0; k < P; ++k)
+      for (int q = 0; q < P; ++q) {
+        const double th = -2.0 * 3.14159265358979323846 * (double)(q * k) / (double)N;
+        tw[k * P + q] = make_float2((float)cos(th), (float)sin(th));
+      }
+  }
+};
+
+// N = 1024 = 16 * 16 * 4 with T = 64 threads per line (E = 16): twice the warps of a 32 x 32
+// four-step and half the registers.  With n = t + 64p, t = a + 4b and k = k1 + 16c + 256d:
+//   W^{nk} = W16^{p k1} . W1024^{t k1} . W16^{b c} . W64^{a c} . W4^{a d}
+// DIT: DFT16 over p | x W1024^{t k1} | exchange | DFT16 over b | x W64^{ac} | exchange | 4 DFT4 over a.
+// DIF runs the mirror stages.  D1: thread t = 4 k1 + g holds k = k1 + 64 g + 16 r + 256 d in
+// register d + 4r.  Exchange layouts are XOR-swizzled so that both the writing and the reading
+// pattern of each exchange are shared-memory-bank-conflict free (one 8 KB buffer per line).
+struct Eng1024 {
+  static constexpr int N = 1024, T = 64, E = 16;
+  static constexpr int EX = 1024;
+  static constexpr int T2 = 1024;         // W64^{ac} at tw[T2 + 17a + c]
+  static constexpr int TW = 1024 + 72;
+  __device__ __forceinline__ static int e1(int k1, int t) { return k1 * 64 + (t ^ ((k1 & 3) << 2)); }
+  __device__ __forceinline__ static int e2(int k1, int a, int c) {
+    return k1 * 64 + 16 * a + ((((c >> 2) ^ a) << 2) | ((c & 3) ^ (k1 & 3)));
+  }
+  __device__ __forceinline__ static int idx(int dist, int t, int k) {
+    return dist ? (t >> 2) + 64 * (t & 3) + 16 * (k >> 2) + 256 * (k & 3) : t + 64 * k;
+  }
+  __device__ __forceinline__ static void sync_line(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+  __device__ __forceinline__ static void dit(float2 (&x)[16], float2* __restrict__ ex, int t,
+                                            const float2* __restrict__ tw, int bid) {
+    DftReg<16>::run(x);  // over p -> k1
+#pragma unroll
+    for (int k1 = 1; k1 < 16; ++k1) x[k1] = cmul(x[k1], tw[e1(k1, t)]);
+    sync_line(bid);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) ex[e1(k1, t)] = x[k1];
+    sync_line(bid);
+    const int k1u = t >> 2, a = t & 3;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) x[b] = ex[e1(k1u, a + 4 * b)];
+    DftReg<16>::run(x);  // over b -> c
+#pragma unroll
+    for (int c = 1; c < 16; ++c) x[c] = cmul(x[c], tw[T2 + 17 * a + c]);
+    sync_line(bid);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) ex[e2(k1u, a, c)] = x[c];
+    sync_line(bid);
+    const int g = t & 3;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int aa = 0; aa < 4; ++aa) x[aa + 4 * r] = ex[e2(k1u, aa, 4 * g + r)];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) dft4(x[4 * r], x[4 * r + 1], x[4 * r + 2], x[4 * r + 3]);  // over a -> d
+  }
+
+  __device__ __forceinline__ static void dif(float2 (&x)[16], float2* __restrict__ ex, int t,
+                                            const float2* __restrict__ tw, int bid) {
+    const int k1w = t >> 2, g = t & 3;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      dft4(x[4 * r], x[4 * r + 1], x[4 * r + 2], x[4 * r + 3]);  // over d -> a
+#pragma unroll
+      for (int aa = 1; aa < 4; ++aa) x[aa + 4 * r] = cmul(x[aa + 4 * r], tw[T2 + 17 * aa + 4 * g + r]);
+    }
+    sync_line(bid);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int aa = 0; aa < 4; ++aa) ex[e2(k1w, aa, 4 * g + r)] = x[aa + 4 * r];
+    sync_line(bid);
+    const int a = t & 3;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) x[c] = ex[e2(k1w, a, c)];
+    DftReg<16>::run(x);  // over c -> b
+#pragma unroll
+    for (int b = 0; b < 16; ++b) x[b] = cmul(x[b], tw[e1(k1w, a + 4 * b)]);
+    sync_line(bid);
+#pragma unroll
+    for (int b = 0; b < 16; ++b) ex[e1(k1w, a + 4 * b)] = x[b];
+    sync_line(bid);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) x[k1] = ex[e1(k1, t)];
+    DftReg<16>::run(x);  // over k1 -> p
+  }
+
+  static void fill(float2* tw) {
+    const double pi2 = 2.0 * 3.14159265358979323846;
+    for (int i = 0; i < TW; ++i) tw[i] = make_float2(0.f, 0.f);
+    for (int k1 = 0; k1 < 16; ++k1)
+      for (int t = 0; t < 64; ++t) {
+        const double th = -pi2 * (double)(t * k1) / 1024.0;
+        tw[k1 * 64 + (t ^ ((k1 & 3) << 2))] = make_float2((float)cos(th), (float)sin(th));
+      }
+    for (int a = 0; a < 4; ++a)
+      for (int c = 0; c < 16; ++c) {
+        const double th = -pi2 * (double)(a * c) / 64.0;
+        tw[T2 + 17 * a + c] = make_float2((float)cos(th), (float)sin(th));
+      }
+  }
+};
+
+template <int N> struct EngOf;
+template <int N> struct EngThreads { static constexpr int v = N == 64 ? 8 : (N == 256 ? 16 : 32); };
+#ifdef PTYCHO_ENG1024_3STAGE
+template <> struct EngThreads<1024> { static constexpr int v = 64; };
+#endif
+template <> struct EngOf<64> { using type = EngFour<8>; };
+template <> struct EngOf<256> { using type = EngFour<16>; };
+// The 16x16x4 / 64-thread engine doubles the warps but measured slower on B200 (two exchanges
+// per transform saturate the shared-memory pipe: 22.9 us vs 20.6 us per backward pass, ncu
+// profiles/round1.md); the 32 x 32 four-step is used.  Eng1024 stays selectable for experiments.
+#ifdef PTYCHO_ENG1024_3STAGE
+template <> struct EngOf<1024> { using type = Eng1024; };
+#else
+template <> struct EngOf<1024> { using type = EngFour<32>; };
+#endif
+
+size_t twiddle_table_size(int n) {
+  switch (n) {
+    case 64: return EngFour<8>::TW;
+    case 256: return EngFour<16>::TW;
+    case 1024: return EngOf<1024>::type::TW;
+    default: return 0;
+  }
+}
+
+void fill_twiddles(int n, float2* tw) {
+  switch (n) {
+    case 64: EngFour<8>::fill(tw); break;
+    case 256: EngFour<16>::fill(tw); break;
+    case 1024: EngOf<1024>::type::fill(tw); break;
+    default: break;
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -218,11 +399,12 @@ __device__ __forceinline__ LineLoc line_loc(const PassArgs& a, int ax, int line,
 // Shared-memory carve-up of a pass CTA.
 template <int N, int KIND>
 struct Smem {
-  static constexpr int P = Geo<N>::P, Q = Geo<N>::Q, L = LINES_PER_CTA;
-  static constexpr size_t tw = 0;                                    // N float2 twiddles
-  static constexpr size_t ht = tw + N * 8;                           // H_1/N, m = 0..N/2 (even in m)
+  using ENG = typename EngOf<N>::type;
+  static constexpr int L = LINES_PER_CTA;
+  static constexpr size_t tw = 0;                                    // twiddles (engine layout)
+  static constexpr size_t ht = tw + (size_t)ENG::TW * 8;             // H_1/N, m = 0..N/2 (even in m)
   static constexpr size_t lines = ht + (N / 2 + 2) * 8;
-  static constexpr size_t ex_b = (size_t)P * (Q + 1) * 8;            // per line
+  static constexpr size_t ex_b = (size_t)ENG::EX * 8;                // exchange buffer per line
   static constexpr size_t st_b = kind_grad(KIND) ? (size_t)N * 8 : 0;  // stash prefetch per line
   static constexpr size_t v_b = (kind_transmit(KIND) || kind_grad(KIND) || KIND == K_TURN) ? (size_t)N * 4 : 0;
   static constexpr size_t acc_b = kind_grad(KIND) ? (size_t)N * 4 : 0;  // AccBuf prefetch per line
@@ -232,15 +414,17 @@ struct Smem {
 };
 
 template <int N, int KIND>
-__global__ void __launch_bounds__(LINES_PER_CTA * Geo<N>::Q, 2)
+__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2)
 pass_kernel(const PassArgs a) {
-  constexpr int P = Geo<N>::P, Q = Geo<N>::Q, L = LINES_PER_CTA;
+  using ENG = typename EngOf<N>::type;
+  constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
   constexpr Plan PL = plan_of(KIND);
   using SM = Smem<N, KIND>;
   extern __shared__ __align__(16) unsigned char smem[];
   float2* tw = (float2*)(smem + SM::tw);
   float2* ht = (float2*)(smem + SM::ht);
   const int lw = threadIdx.x / Q, q = threadIdx.x % Q;
+  const int bid = 1 + lw;  // named barrier of this line (engines with T > 32)
   const int line = blockIdx.x * L + lw;
   unsigned char* lbase = smem + SM::lines + lw * SM::per_line;
   float2* ex = (float2*)lbase;
@@ -249,18 +433,19 @@ pass_kernel(const PassArgs a) {
   float* pacc = (float*)(lbase + SM::ex_b + SM::st_b + SM::v_b);  // prefetched AccBuf row (GRAD)
 
   // ---- before the grid dependency: tables, and prefetches of data written >= 2 kernels ago
-  for (int e = threadIdx.x; e < N; e += L * Q) tw[e] = __ldg(a.wtab + e);
-  for (int e = threadIdx.x; e <= N / 2; e += L * Q) ht[e] = __ldg(a.htab + e);
+  // tables: asynchronous copies (no register round trip); waited for with the other prefetches
+  for (int e = threadIdx.x; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
+  for (int e = threadIdx.x; e < N / 4 + 1; e += L * Q) cp_async16((float4*)ht + e, (const float4*)a.htab + e);
+  cp_async_commit();  // group 1: tables
   constexpr bool FIRST = kind_first(KIND);
-  int i = 0;
-  if constexpr (!FIRST) i = *a.cursor;
+  int4 pd;  // probe descriptor written >= 2 kernels ago (by the previous probe's last pass)
+  if constexpr (!FIRST) pd = *a.desc;
   if constexpr (FIRST) {
     griddep_wait();
     griddep_launch();
-    i = *a.cursor;
+    pd = *a.desc;
   }
-  const int2 ctr = a.centers[i];
-  const int wy0 = ctr.x - N / 2, wx0 = ctr.y - N / 2;
+  const int i = pd.x, wy0 = pd.y, wx0 = pd.z;
   const int ax = a.s & 1;
   LineLoc LL = line_loc(a, ax, line, wy0, wx0);
   if constexpr (kind_transmit(KIND) || kind_grad(KIND)) {
@@ -304,15 +489,24 @@ pass_kernel(const PassArgs a) {
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = src[Q * k];
   }
-  __syncthreads();  // tables visible
+  asm volatile("cp.async.wait_group 1;" ::: "memory");  // tables landed (row prefetches may not have)
+  __syncthreads();
 
   float part = 0.f;  // loss partial (RESID)
-  auto step = [&](int st) {
+  // dist: distribution of the registers when the step runs (0 = natural D0, 1 = engine's D1)
+  auto step = [&](int st, int dist) {
     if ((has_step(PL, S_HC_FWD) && st == S_HC_FWD) || (has_step(PL, S_HC_ADJ) && st == S_HC_ADJ)) {
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        // H_1 depends on m_u^2 only: u = q+Qk for k < P/2, else N-u = Q(P-k) - q (P == Q)
-        const float2 h = ht[k < P / 2 ? q + Q * k : Q * (P - k) - q];
+        // H_1 depends on m_u^2 only: look up min(u, N - u)
+        int m;
+        if constexpr (ENG::T * ENG::T == N) {  // four-step, D1 == D0: u = q + Qk
+          m = k < P / 2 ? q + Q * k : Q * (P - k) - q;
+        } else {
+          const int u = ENG::idx(dist, q, k);
+          m = u <= N / 2 ? u : N - u;
+        }
+        const float2 h = ht[m];
         const float2 y = x[k];
         // conj(H) conj(y) = conj(H y) ;  H conj(y)
         if (st == S_HC_FWD) x[k] = make_float2(h.x * y.x - h.y * y.y, -(h.x * y.y + h.y * y.x));
@@ -329,7 +523,7 @@ pass_kernel(const PassArgs a) {
       for (int k = 0; k < P; ++k) {
         const float v = pv[q + Q * k];
         float sn, cs;
-        sincospif(a.sigma_pi * v, &sn, &cs);  // exp(i sigma v): exact reduction, no slow path
+        sincos_t(a.sigma * v, &sn, &cs);
         float2 y = x[k];
         if (PL.transmit_cp) y.y = -y.y;
         x[k] = cmul(y, make_float2(cs, sn));
@@ -338,13 +532,13 @@ pass_kernel(const PassArgs a) {
     } else if (has_step(PL, S_RESID) && st == S_RESID) {
       // X = raw 2-D DFT (N x true F phi_{S-1}); |Psi| = |X|/N (App. A: |H| = 1)
       cp_async_wait_all();
-      __syncwarp();
+      ENG::sync_line(bid);
       const float invn = 1.0f / (float)N;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         const float m = sqrtf(x[k].x * x[k].x + x[k].y * x[k].y);
         const float mag = m * invn;
-        const float r = mag - pv[q + Q * k];
+        const float r = mag - pv[ENG::idx(dist, q, k)];
         part += r * r;
         // chi_Psi = r Psi/|Psi| (0 where |Psi| <= thr, reading #30), /N for the two unnormalised
         // inverse line transforms; conjugated to start the inverse as conj o F o conj.
@@ -353,9 +547,9 @@ pass_kernel(const PassArgs a) {
       }
     } else if (has_step(PL, S_SIMUL) && st == S_SIMUL) {
       const float invn = 1.0f / (float)N;
-      float* am = a.amp + (size_t)i * N * N + (size_t)line * N + q;
+      float* am = a.amp + (size_t)i * N * N + (size_t)line * N;
 #pragma unroll
-      for (int k = 0; k < P; ++k) am[Q * k] = sqrtf(x[k].x * x[k].x + x[k].y * x[k].y) * invn;
+      for (int k = 0; k < P; ++k) am[ENG::idx(dist, q, k)] = sqrtf(x[k].x * x[k].x + x[k].y * x[k].y) * invn;
     } else if (has_step(PL, S_GRAD) && st == S_GRAD) {
       // chi_phi = conj(y).  g_s = 2 sigma Im(chi conj(phi_s)) (App. A); on win ^ R_k:
       // AccBuf += g (Alg. 1 step 7), V -= alpha g (step 8); chi <- conj(t_s) chi with t_s from
@@ -364,31 +558,30 @@ pass_kernel(const PassArgs a) {
       float* vrow = a.V + so;
       float* arow = a.acc + so;
       cp_async_wait_all();
-      __syncwarp();
+      ENG::sync_line(bid);
       const float two_sigma = 2.0f * a.sigma;
       const bool exporting = a.gexport != nullptr;  // debug: write g instead of updating
-      float* vbase = vrow + LL.pos0 + q;
-      float* abase = arow + LL.pos0 + q;
-      const int lim = LL.ok ? LL.plim - LL.pos0 - q : 0;  // element k valid iff 0 <= Qk + pos0 + q < plim
-      const int low = -(LL.pos0 + q);
+      const int lim = LL.ok ? LL.plim : 0;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         if ((k & 7) == 0) asm volatile("" ::: "memory");
-        const int j = q + Q * k;
+        const int j = ENG::idx(dist, q, k);
+        const int p = LL.pos0 + j;
         const float2 ph = pst[j];
         const float2 chi = make_float2(x[k].x, -x[k].y);
         const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
         const float v = pv[j];
-        if (!exporting && Q * k >= low && Q * k < lim) {
-          abase[Q * k] = pacc[j] + g;
-          vbase[Q * k] = v - a.alpha * g;
+        if (!exporting && (unsigned)p < (unsigned)lim) {
+          arow[p] = pacc[j] + g;
+          vrow[p] = v - a.alpha * g;
         }
         pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
         float sn, cs;
-        sincospif(a.sigma_pi * v, &sn, &cs);
+        sincos_t(a.sigma * v, &sn, &cs);
         x[k] = cmulc(chi, make_float2(cs, sn));
       }
       if (exporting) {
+        ENG::sync_line(bid);
         float* o = a.gexport + (size_t)a.s * N * N;
 #pragma unroll 4
         for (int k = 0; k < P; ++k) {
@@ -405,10 +598,12 @@ pass_kernel(const PassArgs a) {
     if (f == 1) st = PL.pre[1];
     if (f == 2) st = PL.pre[2];
     if (f == 3) st = PL.pre[3];
-    step(st);
-    fft_fwd<N>(x, ex, q, tw);
+    step(st, f & 1);
+    if (f & 1) ENG::dif(x, ex, q, tw, bid);
+    else ENG::dit(x, ex, q, tw, bid);
   }
-  step(PL.post);
+  step(PL.post, PL.nf & 1);
+  constexpr int DIST_OUT = PL.nf & 1;
 
   if constexpr (KIND == K_TURN) {
 #pragma unroll
@@ -429,23 +624,31 @@ pass_kernel(const PassArgs a) {
   }
   constexpr int STORE = kind_store(KIND);
   if constexpr (STORE == 1) {
-    // out[j][line]: stage the CTA's L lines, then write L consecutive complex per output row.
+    // out[j][line]: stage the CTA's L = 4 lines as 32-B rows [j][4] (element l stored at
+    // l ^ ((j >> 2) & 3): conflict-free column writes), then write 16-B chunks of each output
+    // row segment (L consecutive complex64 = one 32-B sector).
+    static_assert(L == 4, "staging assumes 4 lines per CTA");
     __syncthreads();
     float2* stg = (float2*)(smem + SM::lines);
 #pragma unroll
-    for (int k = 0; k < P; ++k) stg[(q + Q * k) * (L + 1) + lw] = x[k];
+    for (int k = 0; k < P; ++k) {
+      const int j = ENG::idx(DIST_OUT, q, k);
+      stg[j * 4 + (lw ^ ((j >> 2) & 3))] = x[k];
+    }
     __syncthreads();
     float2* dst = a.out + (size_t)blockIdx.x * L;
 #pragma unroll 4
-    for (int e = threadIdx.x; e < N * L; e += L * Q) {
-      const int j = e / L, l = e - j * L;
-      dst[(size_t)j * N + l] = stg[j * (L + 1) + l];
+    for (int e = threadIdx.x; e < N * 2; e += L * Q) {
+      const int j = e >> 1, c = e & 1, sw = (j >> 2) & 3;
+      float4 v = *(const float4*)(stg + j * 4 + 2 * c);
+      if (sw & 1) v = make_float4(v.z, v.w, v.x, v.y);
+      *(float4*)(dst + (size_t)j * N + 2 * (c ^ (sw >> 1))) = v;
     }
   }
   if constexpr (STORE == 2) {
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      const int j = q + Q * k;
+      const int j = ENG::idx(DIST_OUT, q, k);
       const size_t o = a.natural_transposed ? (size_t)j * N + line : (size_t)line * N + j;
       a.natural_out[o] = x[k];
     }
@@ -456,9 +659,11 @@ pass_kernel(const PassArgs a) {
     if (threadIdx.x == 0) {
       __threadfence();
       const unsigned prev = atomicAdd(a.done, 1u);
-      if (prev == gridDim.x - 1) {
+      if (prev == gridDim.x - 1) {  // every CTA has read *desc: advance to the next probe
         *a.done = 0u;
-        atomicAdd(a.cursor, 1);
+        const int nx = pd.x + 1 < a.n_probes ? pd.x + 1 : pd.x;
+        const int2 c = a.centers[nx];
+        *a.desc = make_int4(pd.x + 1, c.x - N / 2, c.y - N / 2, 0);
         __threadfence();
       }
     }
@@ -477,7 +682,7 @@ static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) 
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(N / LINES_PER_CTA);
-  cfg.blockDim = dim3(LINES_PER_CTA * Geo<N>::Q);
+  cfg.blockDim = dim3(LINES_PER_CTA * EngOf<N>::type::T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -637,6 +842,17 @@ cudaError_t launch_amp_load(float* dst, const float* src, int count, int n, int 
     amp_load_kernel<<<dim3(n, nc), 256, 0, stream>>>(dst + (long long)c0 * n * n, src + (long long)c0 * n * n, n,
                                                      shift, intensity, transpose);
   }
+  return cudaGetLastError();
+}
+
+__global__ void set_desc_kernel(int4* desc, const int2* centers, int v, int nk, int n) {
+  const int j = v < nk ? v : (nk > 0 ? nk - 1 : 0);
+  const int2 c = centers[j];
+  *desc = make_int4(v, c.x - n / 2, c.y - n / 2, 0);
+}
+
+cudaError_t launch_set_desc(int4* desc, const int2* centers, int v, int nk, int n, cudaStream_t stream) {
+  set_desc_kernel<<<1, 1, 0, stream>>>(desc, centers, v, nk, n);
   return cudaGetLastError();
 }
 
