@@ -150,6 +150,21 @@ struct EngFour {
     __syncwarp();
     DftReg<P>::run(x);
   }
+  // same transform with the thread's P twiddles W_N^{qk} held in registers (loaded once per pass)
+  __device__ __forceinline__ static void fft_r(float2 (&x)[E], float2* __restrict__ ex, int q,
+                                              const float2 (&twr)[P]) {
+    DftReg<P>::run(x);
+#pragma unroll
+    for (int k = 1; k < P; ++k) x[k] = cmul(x[k], twr[k]);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < P; ++k) ex[k * (P + 1) + q] = x[k];
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < P; ++n) x[n] = ex[q * (P + 1) + n];
+    __syncwarp();
+    DftReg<P>::run(x);
+  }
   __device__ __forceinline__ static void dit(float2 (&x)[E], float2* ex, int t, const float2* tw, int) {
     fft(x, ex, t, tw);
   }
@@ -401,8 +416,9 @@ template <int N, int KIND>
 struct Smem {
   using ENG = typename EngOf<N>::type;
   static constexpr int L = LINES_PER_CTA;
+  static constexpr bool TW_REG = (ENG::T * ENG::T == N);               // twiddles in registers
   static constexpr size_t tw = 0;                                    // twiddles (engine layout)
-  static constexpr size_t ht = tw + (size_t)ENG::TW * 8;             // H_1/N, m = 0..N/2 (even in m)
+  static constexpr size_t ht = tw + (TW_REG ? 0 : (size_t)ENG::TW * 8);  // H_1/N, m = 0..N/2
   static constexpr size_t lines = ht + (N / 2 + 2) * 8;
   static constexpr size_t ex_b = (size_t)ENG::EX * 8;                // exchange buffer per line
   static constexpr size_t st_b = kind_grad(KIND) ? (size_t)N * 8 : 0;  // stash prefetch per line
@@ -432,9 +448,17 @@ pass_kernel(const PassArgs a) {
   float* pv = (float*)(lbase + SM::ex_b + SM::st_b);        // prefetched V row / amplitude row
   float* pacc = (float*)(lbase + SM::ex_b + SM::st_b + SM::v_b);  // prefetched AccBuf row (GRAD)
 
+  // four-step engines keep the thread's twiddles in registers (no shared-memory table)
+  constexpr bool TW_REG = (ENG::T * ENG::T == N);
+  float2 twr[TW_REG ? P : 1];
+  if constexpr (TW_REG) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) twr[k] = __ldg(a.wtab + k * Q + q);
+  }
   // ---- before the grid dependency: tables, and prefetches of data written >= 2 kernels ago
   // tables: asynchronous copies (no register round trip); waited for with the other prefetches
-  for (int e = threadIdx.x; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
+  if constexpr (!TW_REG)
+    for (int e = threadIdx.x; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
   for (int e = threadIdx.x; e < N / 4 + 1; e += L * Q) cp_async16((float4*)ht + e, (const float4*)a.htab + e);
   cp_async_commit();  // group 1: tables
   constexpr bool FIRST = kind_first(KIND);
@@ -599,8 +623,12 @@ pass_kernel(const PassArgs a) {
     if (f == 2) st = PL.pre[2];
     if (f == 3) st = PL.pre[3];
     step(st, f & 1);
-    if (f & 1) ENG::dif(x, ex, q, tw, bid);
-    else ENG::dit(x, ex, q, tw, bid);
+    if constexpr (TW_REG) {
+      ENG::fft_r(x, ex, q, twr);
+    } else {
+      if (f & 1) ENG::dif(x, ex, q, tw, bid);
+      else ENG::dit(x, ex, q, tw, bid);
+    }
   }
   step(PL.post, PL.nf & 1);
   constexpr int DIST_OUT = PL.nf & 1;
