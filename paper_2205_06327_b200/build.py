@@ -33,18 +33,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = True, defines=(), out=None) -> str:
+    """defines / out: experimental variants (e.g. ["PTYCHO_MIN2"], "lib/libptycho_a.so")."""
+    lib_out = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     inc, libdir = nccl_dirs()
     nvcc = os.environ.get("NVCC", "nvcc")
     common = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
+    common += ["-D" + d for d in defines]
+    tag = "" if out is None else "_" + os.path.basename(out).replace(".so", "")
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
+        obj = os.path.join(LIBDIR, src.replace(".cu", tag + ".o"))
         cmd = [nvcc] + common + ["-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
@@ -53,12 +57,12 @@ def build(force: bool = False, verbose: bool = True) -> str:
     for p in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
-    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-L", libdir, "-l:libnccl.so.2",
+    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib_out] + objs + ["-L", libdir, "-l:libnccl.so.2",
                                                     "-Xlinker", "-rpath=" + libdir, "--cudart", "static"]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.check_call(link)
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":

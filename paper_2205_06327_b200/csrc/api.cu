@@ -707,6 +707,8 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   a.sigma_pi = (float)((double)ctx->cfg.sigma / M_PI);
   a.alpha = ctx->cfg.alpha;
   a.thr = (float)(ctx->cfg.tau * ctx->probe_norm / ctx->cfg.n);
+  // >= 4 tile chains share the GPU: prefer the forward-pass build with room for more CTAs
+  a.high_occupancy = ctx->local.size() >= 4 ? 1 : 0;
   return a;
 }
 

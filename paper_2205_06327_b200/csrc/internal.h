@@ -37,6 +37,7 @@ struct PassArgs {
   int advance;              // last block advances *desc to the next probe when done
   int n_probes;             // probes of this tile (desc stops at the last one)
   int natural_transposed;   // debug store: lines are columns (1) or rows (0)
+  int high_occupancy;       // forward passes built for 3 CTAs/SM (many concurrent tile chains)
 };
 
 enum PassKind : int {

@@ -22,6 +22,7 @@
 #include "internal.h"
 #include "twiddle32.h"
 
+
 namespace ptycho {
 
 // ------------------------------------------------------------------------------------------
@@ -110,7 +111,8 @@ template <> struct DftReg<4> {
 // (about 1 ulp, no range reduction -- sigma V is a small phase for any physical potential),
 // sincospi with its exact reduction otherwise.
 __device__ __forceinline__ void sincos_t(float x, float* sn, float* cs) {
-  if (fabsf(x) <= 0.785398163f) {
+  // warp-uniform branch: a per-lane branch gets if-converted and evaluates both paths
+  if (__all_sync(0xffffffffu, fabsf(x) <= 0.785398163f)) {
     const float z = x * x;
     *sn = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * x, x);
     *cs = fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f), z * z,
@@ -429,8 +431,13 @@ struct Smem {
   static constexpr size_t total = lines + (per_line * L > stage_b ? per_line * L : stage_b);
 };
 
-template <int N, int KIND>
-__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2)
+// MINB: CTAs per SM the register allocation must allow.  2: the single-chain-latency build
+// (a probe chain alone on the GPU: 2.65 ms/probe at N = 1024, S = 100); 3: forward passes at
+// <= 168 registers leave room for CTAs of other tiles' chains (8 concurrent tiles: +7%
+// probes/s, but a lone chain runs 12% slower).  The host picks per context (api.cu).  Backward
+// passes always use 2 (they spill at 168).  Both builds execute the same arithmetic.
+template <int N, int KIND, int MINB>
+__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KIND) ? 2 : MINB)
 pass_kernel(const PassArgs a) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
@@ -698,9 +705,9 @@ pass_kernel(const PassArgs a) {
   }
 }
 
-template <int N, int KIND>
+template <int N, int KIND, int MINB>
 static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) {
-  auto kern = pass_kernel<N, KIND>;
+  auto kern = pass_kernel<N, KIND, MINB>;
   const size_t smem = Smem<N, KIND>::total;
   static bool attr_set = false;
   if (!attr_set) {
@@ -721,22 +728,27 @@ static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) 
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int N>
-static cudaError_t launch_pass_n(PassKind kind, const PassArgs& a, cudaStream_t s, bool pdl) {
+template <int N, int MINB>
+static cudaError_t launch_pass_nm(PassKind kind, const PassArgs& a, cudaStream_t s, bool pdl) {
   switch (kind) {
-    case K_FWD_FIRST_PROP: return launch_one<N, K_FWD_FIRST_PROP>(a, s, pdl);
-    case K_FWD_FIRST_FFT: return launch_one<N, K_FWD_FIRST_FFT>(a, s, pdl);
-    case K_FWD_MID: return launch_one<N, K_FWD_MID>(a, s, pdl);
-    case K_FWD_LAST: return launch_one<N, K_FWD_LAST>(a, s, pdl);
-    case K_TURN: return launch_one<N, K_TURN>(a, s, pdl);
-    case K_SIMULATE: return launch_one<N, K_SIMULATE>(a, s, pdl);
-    case K_BWD_LAST_PROP: return launch_one<N, K_BWD_LAST_PROP>(a, s, pdl);
-    case K_BWD_LAST_END: return launch_one<N, K_BWD_LAST_END>(a, s, pdl);
-    case K_BWD_MID: return launch_one<N, K_BWD_MID>(a, s, pdl);
-    case K_BWD_END: return launch_one<N, K_BWD_END>(a, s, pdl);
-    case K_EXIT_COMPLETE: return launch_one<N, K_EXIT_COMPLETE>(a, s, pdl);
+    case K_FWD_FIRST_PROP: return launch_one<N, K_FWD_FIRST_PROP, MINB>(a, s, pdl);
+    case K_FWD_FIRST_FFT: return launch_one<N, K_FWD_FIRST_FFT, MINB>(a, s, pdl);
+    case K_FWD_MID: return launch_one<N, K_FWD_MID, MINB>(a, s, pdl);
+    case K_FWD_LAST: return launch_one<N, K_FWD_LAST, MINB>(a, s, pdl);
+    case K_TURN: return launch_one<N, K_TURN, MINB>(a, s, pdl);
+    case K_SIMULATE: return launch_one<N, K_SIMULATE, MINB>(a, s, pdl);
+    case K_BWD_LAST_PROP: return launch_one<N, K_BWD_LAST_PROP, 2>(a, s, pdl);
+    case K_BWD_LAST_END: return launch_one<N, K_BWD_LAST_END, 2>(a, s, pdl);
+    case K_BWD_MID: return launch_one<N, K_BWD_MID, 2>(a, s, pdl);
+    case K_BWD_END: return launch_one<N, K_BWD_END, 2>(a, s, pdl);
+    case K_EXIT_COMPLETE: return launch_one<N, K_EXIT_COMPLETE, MINB>(a, s, pdl);
     default: return cudaErrorInvalidValue;
   }
+}
+
+template <int N>
+static cudaError_t launch_pass_n(PassKind kind, const PassArgs& a, cudaStream_t s, bool pdl) {
+  return a.high_occupancy ? launch_pass_nm<N, 3>(kind, a, s, pdl) : launch_pass_nm<N, 2>(kind, a, s, pdl);
 }
 
 cudaError_t launch_pass(int n, PassKind kind, const PassArgs& a, cudaStream_t stream, bool pdl) {

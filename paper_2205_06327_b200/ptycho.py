@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libptycho.so")
+LIB_PATH = os.environ.get("PTYCHO_LIB", os.path.join(_HERE, "lib", "libptycho.so"))  # override: A/B builds
 
 PTYCHO_F_EXACT_WINDOW = 1
 PTYCHO_AMP_DC_CENTERED = 1
