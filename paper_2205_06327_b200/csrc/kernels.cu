@@ -155,6 +155,9 @@ struct EngFour {
   // same transform with the thread's P twiddles W_N^{qk} held in registers (loaded once per pass)
   __device__ __forceinline__ static void fft_r(float2 (&x)[E], float2* __restrict__ ex, int q,
                                               const float2 (&twr)[P]) {
+#ifdef PTYCHO_EXPERIMENT_NO_FFT
+    return;  // timing experiment only: everything but the transforms
+#endif
     DftReg<P>::run(x);
 #pragma unroll
     for (int k = 1; k < P; ++k) x[k] = cmul(x[k], twr[k]);
