@@ -186,14 +186,17 @@ def _recon_problem():
     return d, probe, vt, centers, amps
 
 
-@pytest.mark.parametrize("grid,period,iters", [((1, 1), 0, 2), ((2, 3), 0, 2), ((2, 3), 3, 1), ((3, 2), 4, 2)])
-def test_reconstruction_matches_oracle(grid, period, iters):
+@pytest.mark.parametrize("grid,period,iters,halo", [((1, 1), 0, 2, 32), ((2, 3), 0, 2, 32), ((2, 3), 3, 1, 32),
+                                                    ((3, 2), 4, 2, 32), ((2, 3), 0, 2, 12), ((3, 2), 1, 1, 7)])
+def test_reconstruction_matches_oracle(grid, period, iters, halo):
+    """halo 32 = N/2 (exact window); halo 12 / 7 = the paper's circle-halo mode (reading #13:
+    windows are zero-extended past R_k, an approximation both sides implement identically)."""
     d, probe, vt, centers, amps = _recon_problem()
     v0 = (0.5 * vt).astype(np.float32)
     alpha = 1.0
     ref, losses, _, _ = O.reconstruct(v0.astype(np.float64), probe, amps.astype(np.float64), centers, d, grid[0],
-                                      grid[1], d["n"] // 2, iters, alpha=alpha, period=period)
-    p = make(d, rows=grid[0], cols=grid[1], alpha=alpha, period=period)
+                                      grid[1], halo, iters, alpha=alpha, period=period)
+    p = make(d, rows=grid[0], cols=grid[1], halo=halo, alpha=alpha, period=period)
     p.set_scan(centers)
     p.allocate_workspace()
     p.set_probe(probe.astype(np.complex64))
@@ -204,7 +207,7 @@ def test_reconstruction_matches_oracle(grid, period, iters):
     out = p.stitch()
     err = rel(out, ref)
     derr = rel(out - v0, ref - v0)
-    print(f"grid {grid} T={period}: V rel {err:.2e}, dV rel {derr:.2e}, losses {got_losses} vs {losses}")
+    print(f"grid {grid} T={period} halo {halo}: V rel {err:.2e}, dV rel {derr:.2e}, losses {got_losses} vs {losses}")
     assert err <= 1e-4
     assert derr <= 1e-3
     for a, b in zip(got_losses, losses):

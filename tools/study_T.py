@@ -1,0 +1,59 @@
+"""Pass-frequency (T) and halo study on synthetic data (PAPER.md P:446-456,
+Fig. convergence: "once or twice per iteration converges slightly faster than every probe").
+
+F(V) (Eq. 1, summed over the sweep) per iteration for T in {every probe, twice per iteration,
+once per iteration}, in exact-window mode (halo N/2) and the paper's circle-halo mode (small halo,
+zero-extended windows, reading #13), on a 2x2 tile grid.  Writes profiles/round1_T_study.json."""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_2205_06327_b200.ptycho import Ptycho  # noqa: E402
+
+n, s, h, w = 64, 4, 256, 256
+ny = nx = 12
+iters = int(os.environ.get("ITERS", 40))
+alpha = float(os.environ.get("ALPHA", 0.5))
+probe = synth.probe(n, 8.0).astype(np.complex64)
+vt = synth.volume(1, s, h, w)
+centers = synth.scan_centers(h, w, ny, nx)
+
+
+def run(period, halo, grid=(2, 2)):
+    p = Ptycho(n, s, h, w, 0.1, 3.135, alpha=alpha, pass_period=period)
+    p.set_tiles(grid[0], grid[1], halo)
+    p.set_scan(centers)
+    p.allocate_workspace()
+    p.set_probe(probe)
+    p.set_volume(vt)
+    p.simulate_measurements()
+    p.set_volume(None)
+    nmax = max(p.tile_probe_count(k) for k in range(grid[0] * grid[1]))
+    losses = [p.iterate(want_loss=True) for _ in range(iters)]
+    v = p.stitch()
+    err = float(np.linalg.norm(v - vt) / np.linalg.norm(vt))
+    p.close()
+    return nmax, losses, err
+
+
+out = {"config": dict(n=n, slices=s, object=[h, w], probes=ny * nx, grid="2x2", alpha=alpha, iterations=iters,
+                      v0="0", measurements="simulated |G(p, V_true)| (noise-free)"), "runs": []}
+nmax = None
+for halo, mode in [(n // 2, "exact-window"), (12, "circle-halo")]:
+    base = run(0, halo)
+    nmax = base[0]
+    for name, period in [("every probe (T=1)", 1), ("twice per iteration", -(-nmax // 2)), ("once per iteration", 0)]:
+        _, losses, err = base if period == 0 else run(period, halo)
+        out["runs"].append(dict(mode=mode, halo=halo, T=name, period=period, F=losses, rel_err_V=err))
+        print(f"{mode:13s} {name:22s} F[0]={losses[0]:.4e} F[9]={losses[9]:.4e} F[-1]={losses[-1]:.4e} "
+              f"|V-Vtrue|/|Vtrue|={err:.4f}", flush=True)
+single = run(0, n // 2, grid=(1, 1))
+out["runs"].append(dict(mode="single tile", halo=0, T="once per iteration", period=0, F=single[1], rel_err_V=single[2]))
+print(f"{'single tile':13s} {'once per iteration':22s} F[-1]={single[1][-1]:.4e} |V-Vtrue|/|Vtrue|={single[2]:.4f}")
+os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+json.dump(out, open(os.path.join(ROOT, "profiles", "round1_T_study.json"), "w"), indent=1)
