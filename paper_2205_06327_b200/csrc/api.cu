@@ -49,6 +49,7 @@ struct Tile {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev = nullptr;
   cudaGraphExec_t graph = nullptr;
+  std::vector<cudaEvent_t> slab_ev;  // APPP slab pipelining (segment_pipelined)
 };
 
 constexpr size_t ALIGN = 256;
@@ -94,6 +95,7 @@ struct ptycho_ctx_s {
   cudaEvent_t ev_fork = nullptr;
   bool use_graph = true;
   bool use_pdl = true;
+  int slab = 0;  // slices per APPP slab in ptycho_iterate (0 = passes after the whole segment)
 };
 
 static thread_local std::string g_create_err;
@@ -125,8 +127,6 @@ static ptycho_status fail(ptycho_ctx ctx, ptycho_status st, const char* fmt, ...
     if (s_ != PTYCHO_OK) return s_;                                                               \
   } while (0)
 
-static int slices_even(int S) { return (S + 1) / 2; }
-static int slices_odd(int S) { return S / 2; }
 
 // ------------------------------------------------------------------------------------------
 // tiny device helpers launched from here
@@ -153,6 +153,9 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   ctx->stream = (cudaStream_t)cuda_stream;
   if (const char* e = getenv("PTYCHO_NO_GRAPH")) ctx->use_graph = atoi(e) == 0;
   if (const char* e = getenv("PTYCHO_NO_PDL")) ctx->use_pdl = atoi(e) == 0;
+  // APPP slab size: ~S/10 slices (>= 1); PTYCHO_SLAB overrides, 0 disables the pipelining
+  ctx->slab = std::max(1, (cfg->slices + 9) / 10);
+  if (const char* e = getenv("PTYCHO_SLAB")) ctx->slab = std::max(0, atoi(e));
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -181,6 +184,7 @@ extern "C" ptycho_status ptycho_destroy(ptycho_ctx ctx) {
     if (t.graph) cudaGraphExecDestroy(t.graph);
     if (t.stream) cudaStreamDestroy(t.stream);
     if (t.ev) cudaEventDestroy(t.ev);
+    for (cudaEvent_t e : t.slab_ev) cudaEventDestroy(e);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -604,17 +608,21 @@ struct SliceView {
   int rows, cols, nslices;
 };
 
-static SliceView region_view(const Tile& t, float* buf, int parity, int S, int y0, int y1, int x0, int x1) {
+// Region [y0,y1)x[x0,x1) of the slices s in [z0, z1) with s % 2 == parity.
+static SliceView region_view(const Tile& t, float* buf, int parity, int z0, int z1, int y0, int y1, int x0,
+                             int x1) {
   SliceView v;
   v.ss = 2 * t.slice_stride;
-  v.nslices = parity ? slices_odd(S) : slices_even(S);
+  const int s0 = z0 + (((z0 & 1) != parity) ? 1 : 0);
+  v.nslices = s0 < z1 ? (z1 - s0 + 1) / 2 : 0;
+  const long long sb = (long long)s0 * t.slice_stride;
   if (parity == 0) {
-    v.base = buf + (long long)(y0 - t.ey0) * t.pitch0 + (x0 - t.ex0);
+    v.base = buf + sb + (long long)(y0 - t.ey0) * t.pitch0 + (x0 - t.ex0);
     v.ld = t.pitch0;
     v.rows = y1 - y0;
     v.cols = x1 - x0;
   } else {
-    v.base = buf + t.slice_stride + (long long)(x0 - t.ex0) * t.pitch1 + (y0 - t.ey0);
+    v.base = buf + sb + (long long)(x0 - t.ex0) * t.pitch1 + (y0 - t.ey0);
     v.ld = t.pitch1;
     v.rows = x1 - x0;
     v.cols = y1 - y0;
@@ -718,7 +726,8 @@ struct ChainProfile {  // optional per-kind event timing (ptycho_profile_chain)
 };
 
 static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cudaStream_t st,
-                                   ChainProfile* prof = nullptr) {
+                                   ChainProfile* prof = nullptr, std::vector<cudaEvent_t>* slab_ev = nullptr,
+                                   int slab = 0) {
   const int S = ctx->cfg.slices, n = ctx->cfg.n;
   PassArgs a = base_args(ctx, t);
   int pass = 0;
@@ -747,6 +756,8 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
       CK(launch_pass(n, kind, b, st, ctx->use_pdl));
     }
     ++ctx->launches;
+    const bool bwd = kind == K_BWD_LAST_PROP || kind == K_BWD_LAST_END || kind == K_BWD_MID || kind == K_BWD_END;
+    if (slab_ev && bwd && s % slab == 0) CK(cudaEventRecord((*slab_ev)[s / slab], st));
     ++pass;
     return PTYCHO_OK;
   };
@@ -888,13 +899,13 @@ extern "C" ptycho_status ptycho_simulate_measurements(ptycho_ctx ctx) {
 // ------------------------------------------------------------------------------------------
 // APPP passes (Alg. 1 steps 10-13) and the accumulated step (steps 14-16)
 // ------------------------------------------------------------------------------------------
-static ptycho_status hop_local(ptycho_ctx ctx, const Hop& h) {
+static ptycho_status hop_local(ptycho_ctx ctx, const Hop& h, int z0, int z1) {
   const Tile& a = ctx->tiles[h.src];
   const Tile& b = ctx->tiles[h.dst];
-  const int S = ctx->cfg.slices;
   for (int par = 0; par < 2; ++par) {
-    SliceView vs = region_view(a, a.acc, par, S, h.y0, h.y1, h.x0, h.x1);
-    SliceView vd = region_view(b, b.acc, par, S, h.y0, h.y1, h.x0, h.x1);
+    SliceView vs = region_view(a, a.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    SliceView vd = region_view(b, b.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    if (vs.nslices == 0) continue;
     CK(launch_copy2d(vd.base, vd.ld, vd.ss, vs.base, vs.ld, vs.ss, vs.rows, vs.cols, vs.nslices, h.add, ctx->stream));
     ++ctx->launches;
   }
@@ -903,18 +914,17 @@ static ptycho_status hop_local(ptycho_ctx ctx, const Hop& h) {
 
 // Remote hop: the region is moved in slabs of whole slices, packed [slice][rows][cols] per
 // parity (even slices [y][x], odd [x][y]); sender packs + ncclSend, receiver ncclRecv + (add|copy).
-static ptycho_status hop_remote(ptycho_ctx ctx, const Hop& h, bool sender) {
+static ptycho_status hop_remote(ptycho_ctx ctx, const Hop& h, bool sender, int z0, int z1) {
   const Tile& me = ctx->tiles[sender ? h.src : h.dst];
   const int peer = ctx->tiles[sender ? h.dst : h.src].owner;
-  const int S = ctx->cfg.slices;
   const size_t area = (size_t)(h.y1 - h.y0) * (h.x1 - h.x0);
   const int slab = (int)std::max<size_t>(1, ctx->msg_floats / area);
   for (int par = 0; par < 2; ++par) {
-    SliceView v = region_view(me, me.acc, par, S, h.y0, h.y1, h.x0, h.x1);
-    for (int z0 = 0; z0 < v.nslices; z0 += slab) {
-      const int nz = std::min(slab, v.nslices - z0);
+    SliceView v = region_view(me, me.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    for (int q0 = 0; q0 < v.nslices; q0 += slab) {
+      const int nz = std::min(slab, v.nslices - q0);
       const size_t cnt = area * nz;
-      float* base = v.base + (long long)z0 * v.ss;
+      float* base = v.base + (long long)q0 * v.ss;
       const long long per = (long long)v.rows * v.cols;
       if (sender) {
         CK(launch_copy2d(ctx->sendbuf, v.cols, per, base, v.ld, v.ss, v.rows, v.cols, nz, 0, ctx->stream));
@@ -930,28 +940,84 @@ static ptycho_status hop_remote(ptycho_ctx ctx, const Hop& h, bool sender) {
   return PTYCHO_OK;
 }
 
-extern "C" ptycho_status ptycho_appp_passes(ptycho_ctx ctx) {
-  PASS(need_ws(ctx));
-  CK(cudaSetDevice(ctx->device));
+// The four passes on the slices [z0, z1) of every AccBuf (every rank walks the same hop list).
+static ptycho_status appp_range(ptycho_ctx ctx, int z0, int z1) {
   for (const Hop& h : ctx->hops) {
     if (h.y1 <= h.y0 || h.x1 <= h.x0) continue;  // disjoint extended rects: empty message
     const int so = ctx->tiles[h.src].owner, d = ctx->tiles[h.dst].owner;
-    if (so == ctx->rank && d == ctx->rank) PASS(hop_local(ctx, h));
-    else if (so == ctx->rank) PASS(hop_remote(ctx, h, true));
-    else if (d == ctx->rank) PASS(hop_remote(ctx, h, false));
+    if (so == ctx->rank && d == ctx->rank) PASS(hop_local(ctx, h, z0, z1));
+    else if (so == ctx->rank) PASS(hop_remote(ctx, h, true, z0, z1));
+    else if (d == ctx->rank) PASS(hop_remote(ctx, h, false, z0, z1));
   }
   return PTYCHO_OK;
+}
+
+static ptycho_status step_range(ptycho_ctx ctx, int z0, int z1) {
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const long long off = (long long)z0 * t.slice_stride;
+    CK(launch_acc_step(t.V + off, t.acc + off, (long long)(z1 - z0) * t.slice_stride, ctx->cfg.alpha_acc,
+                       ctx->stream));
+    ++ctx->launches;
+  }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_appp_passes(ptycho_ctx ctx) {
+  PASS(need_ws(ctx));
+  CK(cudaSetDevice(ctx->device));
+  return appp_range(ctx, 0, ctx->cfg.slices);
 }
 
 extern "C" ptycho_status ptycho_step(ptycho_ctx ctx) {
   PASS(need_ws(ctx));
   CK(cudaSetDevice(ctx->device));
+  return step_range(ctx, 0, ctx->cfg.slices);
+}
+
+// One pass segment with the APPP chains pipelined by slabs of slices (§8(a) a11):
+// every tile's last probe of the segment runs as direct launches that record an event when its
+// backward pass has finished the lowest slice of each slab (AccBuf of that slab is then final);
+// the passes and the accumulated step of a slab start as soon as every local tile reached it,
+// overlapping the backward passes of the lower slices.
+static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t count) {
+  const int S = ctx->cfg.slices, slab = ctx->slab, nslab = (S + slab - 1) / slab;
+  PASS(fork_tiles(ctx));
+  int64_t maxn = 0;
+  std::vector<int64_t> m(ctx->tiles.size(), 0);
   for (int k : ctx->local) {
     Tile& t = ctx->tiles[k];
-    CK(launch_acc_step(t.V, t.acc, (long long)t.slice_stride * ctx->cfg.slices, ctx->cfg.alpha_acc, ctx->stream));
-    ++ctx->launches;
+    m[k] = std::max<int64_t>(0, std::min<int64_t>(first + count, (int64_t)t.probes.size()) - first);
+    maxn = std::max(maxn, m[k]);
+    if (m[k] > 0) PASS(set_cursor(ctx, t, (int)first, t.stream));
+    PASS(ensure_graph(ctx, t));
+    if ((int)t.slab_ev.size() < nslab) {
+      for (cudaEvent_t e : t.slab_ev) cudaEventDestroy(e);
+      t.slab_ev.assign(nslab, nullptr);
+      for (auto& e : t.slab_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
   }
-  return PTYCHO_OK;
+  for (int64_t j = 0; j < maxn; ++j)
+    for (int k : ctx->local) {
+      Tile& t = ctx->tiles[k];
+      if (j >= m[k]) continue;
+      if (j < m[k] - 1 && t.graph) {
+        CK(cudaGraphLaunch(t.graph, t.stream));
+        ctx->launches += chain_len(S);
+      } else if (j < m[k] - 1) {
+        PASS(enqueue_chain(ctx, t, CHAIN_GRAD, t.stream));
+      } else {
+        PASS(enqueue_chain(ctx, t, CHAIN_GRAD, t.stream, nullptr, &t.slab_ev, slab));
+      }
+    }
+  for (int b = nslab - 1; b >= 0; --b) {
+    for (int k : ctx->local)
+      if (m[k] > 0) CK(cudaStreamWaitEvent(ctx->stream, ctx->tiles[k].slab_ev[b], 0));
+    const int z0 = b * slab, z1 = std::min(S, z0 + slab);
+    PASS(appp_range(ctx, z0, z1));
+    PASS(step_range(ctx, z0, z1));
+  }
+  return join_tiles(ctx);
 }
 
 extern "C" ptycho_status ptycho_iterate(ptycho_ctx ctx, double* loss_out) {
@@ -964,9 +1030,13 @@ extern "C" ptycho_status ptycho_iterate(ptycho_ctx ctx, double* loss_out) {
   const int64_t nseg = ((int64_t)nmax + T - 1) / T;
   if (loss_out) PASS(zero_loss(ctx));
   for (int64_t j = 0; j < nseg; ++j) {
-    PASS(run_probes(ctx, j * T, T, CHAIN_GRAD));
-    PASS(ptycho_appp_passes(ctx));
-    PASS(ptycho_step(ctx));
+    if (ctx->slab > 0) {
+      PASS(segment_pipelined(ctx, j * T, T));
+    } else {
+      PASS(run_probes(ctx, j * T, T, CHAIN_GRAD));
+      PASS(ptycho_appp_passes(ctx));
+      PASS(ptycho_step(ctx));
+    }
   }
   if (loss_out) {
     double local = 0.0;
