@@ -96,6 +96,7 @@ struct ptycho_ctx_s {
   bool use_graph = true;
   bool use_pdl = true;
   int slab = 0;  // slices per APPP slab in ptycho_iterate (0 = passes after the whole segment)
+  bool persist = false;  // run probe chains in the persistent cooperative chain kernel
 };
 
 static thread_local std::string g_create_err;
@@ -156,6 +157,7 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   // APPP slab size: ~S/10 slices (>= 1); PTYCHO_SLAB overrides, 0 disables the pipelining
   ctx->slab = std::max(1, (cfg->slices + 9) / 10);
   if (const char* e = getenv("PTYCHO_SLAB")) ctx->slab = std::max(0, atoi(e));
+  if (const char* e = getenv("PTYCHO_PERSIST")) ctx->persist = atoi(e) != 0;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -851,7 +853,42 @@ static ptycho_status zero_loss(ptycho_ctx ctx) {
   return PTYCHO_OK;
 }
 
+// Probes [first, first + cnt[k]) of every local tile k in one cooperative chain-kernel launch on
+// ctx->stream (tiles in lockstep; a tile with fewer probes idles in the later steps).
+static ptycho_status run_chain_kernel(ptycho_ctx ctx, int64_t first, const std::vector<int64_t>& cnt) {
+  ChainArgs c{};
+  int64_t maxn = 0;
+  int nt = 0;
+  for (int k : ctx->local) {
+    if (nt == MAX_CHAIN_TILES) return fail(ctx, PTYCHO_EARG, "persistent chain: more than %d local tiles", MAX_CHAIN_TILES);
+    Tile& t = ctx->tiles[k];
+    c.t[nt] = base_args(ctx, t);
+    c.t[nt].high_occupancy = 0;
+    c.wf[nt][0] = t.wf[0];
+    c.wf[nt][1] = t.wf[1];
+    c.count[nt] = (int)cnt[k];
+    maxn = std::max(maxn, cnt[k]);
+    ++nt;
+  }
+  if (maxn == 0) return PTYCHO_OK;
+  c.ntiles = nt;
+  c.first = (int)first;
+  c.maxn = (int)maxn;
+  c.S = ctx->cfg.slices;
+  c.bar = (unsigned*)ctx->iscratch;
+  CK(cudaMemsetAsync(ctx->iscratch, 0, sizeof(unsigned), ctx->stream));
+  CK(launch_chain(ctx->cfg.n, c, ctx->stream));
+  ctx->launches += 1;
+  return PTYCHO_OK;
+}
+
 static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, ChainMode mode) {
+  if (mode == CHAIN_GRAD && ctx->persist) {
+    std::vector<int64_t> cnt(ctx->tiles.size(), 0);
+    for (int k : ctx->local)
+      cnt[k] = std::max<int64_t>(0, std::min<int64_t>(first + count, (int64_t)ctx->tiles[k].probes.size()) - first);
+    return run_chain_kernel(ctx, first, cnt);
+  }
   PASS(fork_tiles(ctx));
   int64_t maxn = 0;
   for (int k : ctx->local) {
@@ -982,14 +1019,21 @@ extern "C" ptycho_status ptycho_step(ptycho_ctx ctx) {
 // overlapping the backward passes of the lower slices.
 static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t count) {
   const int S = ctx->cfg.slices, slab = ctx->slab, nslab = (S + slab - 1) / slab;
-  PASS(fork_tiles(ctx));
   int64_t maxn = 0;
   std::vector<int64_t> m(ctx->tiles.size(), 0);
   for (int k : ctx->local) {
-    Tile& t = ctx->tiles[k];
-    m[k] = std::max<int64_t>(0, std::min<int64_t>(first + count, (int64_t)t.probes.size()) - first);
+    m[k] = std::max<int64_t>(0, std::min<int64_t>(first + count, (int64_t)ctx->tiles[k].probes.size()) - first);
     maxn = std::max(maxn, m[k]);
-    if (m[k] > 0) PASS(set_cursor(ctx, t, (int)first, t.stream));
+  }
+  std::vector<int64_t> done(ctx->tiles.size(), 0);  // probes already run by the chain kernel
+  if (ctx->persist) {
+    for (int k : ctx->local) done[k] = m[k] > 0 ? m[k] - 1 : 0;
+    PASS(run_chain_kernel(ctx, first, done));
+  }
+  PASS(fork_tiles(ctx));
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    if (m[k] > 0) PASS(set_cursor(ctx, t, (int)(first + done[k]), t.stream));
     PASS(ensure_graph(ctx, t));
     if ((int)t.slab_ev.size() < nslab) {
       for (cudaEvent_t e : t.slab_ev) cudaEventDestroy(e);
@@ -1000,7 +1044,7 @@ static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t co
   for (int64_t j = 0; j < maxn; ++j)
     for (int k : ctx->local) {
       Tile& t = ctx->tiles[k];
-      if (j >= m[k]) continue;
+      if (j >= m[k] || j < done[k]) continue;
       if (j < m[k] - 1 && t.graph) {
         CK(cudaGraphLaunch(t.graph, t.stream));
         ctx->launches += chain_len(S);

@@ -55,6 +55,18 @@ enum PassKind : int {
   K_COUNT
 };
 
+// Persistent chain kernel (cooperative launch): probes [first, first + count[t]) of every local
+// tile t, all tiles in lockstep, grid barrier between passes.
+constexpr int MAX_CHAIN_TILES = 16;
+struct ChainArgs {
+  PassArgs t[MAX_CHAIN_TILES];         // per tile (s / in / out / advance are set per step)
+  float2* wf[MAX_CHAIN_TILES][2];      // wavefield ping-pong per tile
+  int count[MAX_CHAIN_TILES];          // probes of this segment per tile
+  int ntiles, first, maxn, S;
+  unsigned* bar;                       // grid-barrier counter (zeroed before the launch)
+};
+cudaError_t launch_chain(int n, const ChainArgs& c, cudaStream_t stream);
+
 // Launch one pass kernel (with programmatic dependent launch on `stream`).
 cudaError_t launch_pass(int n, PassKind kind, const PassArgs& a, cudaStream_t stream, bool pdl);
 

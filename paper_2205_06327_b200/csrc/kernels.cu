@@ -434,47 +434,45 @@ struct Smem {
   static constexpr size_t total = lines + (per_line * L > stage_b ? per_line * L : stage_b);
 };
 
-// MINB: CTAs per SM the register allocation must allow.  2: the single-chain-latency build
-// (a probe chain alone on the GPU: 2.65 ms/probe at N = 1024, S = 100); 3: forward passes at
-// <= 168 registers leave room for CTAs of other tiles' chains (8 concurrent tiles: +7%
-// probes/s, but a lone chain runs 12% slower).  The host picks per context (api.cu).  Backward
-// passes always use 2 (they spill at 168).  Both builds execute the same arithmetic.
-template <int N, int KIND, int MINB>
-__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KIND) ? 2 : MINB)
-pass_kernel(const PassArgs a) {
+// The body of one pass for one group of LINES_PER_CTA lines (grp).  PERSIST = false: a
+// standalone kernel in a CUDA-graph/PDL chain (tables loaded here, probe from *desc, input read
+// after griddepcontrol.wait).  PERSIST = true: one step of chain_kernel (tables and twiddles
+// already resident, probe passed in, input written by other CTAs before the grid barrier, read
+// through L2).
+template <int N, int KIND, bool PERSIST>
+__device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4 pd,
+                                          const float2 (&twr)[EngOf<N>::type::T * EngOf<N>::type::T == N
+                                                                  ? EngOf<N>::type::E : 1],
+                                          unsigned char* smem) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
   constexpr Plan PL = plan_of(KIND);
   using SM = Smem<N, KIND>;
-  extern __shared__ __align__(16) unsigned char smem[];
   float2* tw = (float2*)(smem + SM::tw);
   float2* ht = (float2*)(smem + SM::ht);
   const int lw = threadIdx.x / Q, q = threadIdx.x % Q;
   const int bid = 1 + lw;  // named barrier of this line (engines with T > 32)
-  const int line = blockIdx.x * L + lw;
+  const int line = grp * L + lw;
   unsigned char* lbase = smem + SM::lines + lw * SM::per_line;
   float2* ex = (float2*)lbase;
   float2* pst = (float2*)(lbase + SM::ex_b);                // prefetched stash row (GRAD)
   float* pv = (float*)(lbase + SM::ex_b + SM::st_b);        // prefetched V row / amplitude row
   float* pacc = (float*)(lbase + SM::ex_b + SM::st_b + SM::v_b);  // prefetched AccBuf row (GRAD)
-
-  // four-step engines keep the thread's twiddles in registers (no shared-memory table)
   constexpr bool TW_REG = (ENG::T * ENG::T == N);
-  float2 twr[TW_REG ? P : 1];
-  if constexpr (TW_REG) {
-#pragma unroll
-    for (int k = 0; k < P; ++k) twr[k] = __ldg(a.wtab + k * Q + q);
-  }
+  if constexpr (PERSIST) __syncthreads();  // the previous step's staging reads of smem are done
+
   // ---- before the grid dependency: tables, and prefetches of data written >= 2 kernels ago
   // tables: asynchronous copies (no register round trip); waited for with the other prefetches
-  if constexpr (!TW_REG)
-    for (int e = threadIdx.x; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
-  for (int e = threadIdx.x; e < N / 4 + 1; e += L * Q) cp_async16((float4*)ht + e, (const float4*)a.htab + e);
+  if constexpr (!PERSIST) {
+    if constexpr (!TW_REG)
+      for (int e = threadIdx.x; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
+    for (int e = threadIdx.x; e < N / 4 + 1; e += L * Q) cp_async16((float4*)ht + e, (const float4*)a.htab + e);
+  }
   cp_async_commit();  // group 1: tables
   constexpr bool FIRST = kind_first(KIND);
-  int4 pd;  // probe descriptor written >= 2 kernels ago (by the previous probe's last pass)
-  if constexpr (!FIRST) pd = *a.desc;
-  if constexpr (FIRST) {
+  // probe descriptor written >= 2 kernels ago (by the previous probe's last pass)
+  if constexpr (!PERSIST && !FIRST) pd = *a.desc;
+  if constexpr (!PERSIST && FIRST) {
     griddep_wait();
     griddep_launch();
     pd = *a.desc;
@@ -516,12 +514,16 @@ pass_kernel(const PassArgs a) {
     const float2* src = a.probe + (size_t)line * N + q;
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = src[Q * k];
-  } else {
+  } else if constexpr (!PERSIST) {
     griddep_wait();
     griddep_launch();
     const float2* src = a.in + (size_t)line * N + q;
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = src[Q * k];
+  } else {
+    const float2* src = a.in + (size_t)line * N + q;  // written by other SMs last step: bypass L1
+#pragma unroll
+    for (int k = 0; k < P; ++k) x[k] = __ldcg(src + Q * k);
   }
   asm volatile("cp.async.wait_group 1;" ::: "memory");  // tables landed (row prefetches may not have)
   __syncthreads();
@@ -652,7 +654,7 @@ pass_kernel(const PassArgs a) {
     if (threadIdx.x == 0) {
       double tot = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += (double)red[w];
-      a.loss_part[blockIdx.x] += tot;
+      a.loss_part[grp] += tot;
     }
   }
 
@@ -674,7 +676,7 @@ pass_kernel(const PassArgs a) {
       stg[j * 4 + (lw ^ ((j >> 2) & 3))] = x[k];
     }
     __syncthreads();
-    float2* dst = a.out + (size_t)blockIdx.x * L;
+    float2* dst = a.out + (size_t)grp * L;
 #pragma unroll 4
     for (int e = threadIdx.x; e < N * 2; e += L * Q) {
       const int j = e >> 1, c = e & 1, sw = (j >> 2) & 3;
@@ -692,7 +694,7 @@ pass_kernel(const PassArgs a) {
     }
   }
 
-  if (a.advance) {
+  if (!PERSIST && a.advance) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -705,6 +707,162 @@ pass_kernel(const PassArgs a) {
         __threadfence();
       }
     }
+  }
+}
+
+// MINB: CTAs per SM the register allocation must allow.  2: the single-chain-latency build
+// (a probe chain alone on the GPU: 2.65 ms/probe at N = 1024, S = 100); 3: forward passes at
+// <= 168 registers leave room for CTAs of other tiles' chains (8 concurrent tiles: +7%
+// probes/s, but a lone chain runs 12% slower).  The host picks per context (api.cu).  Backward
+// passes always use 2 (they spill at 168).  Both builds execute the same arithmetic.
+template <int N, int KIND, int MINB>
+__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KIND) ? 2 : MINB)
+pass_kernel(const PassArgs a) {
+  using ENG = typename EngOf<N>::type;
+  constexpr int P = ENG::E, Q = ENG::T;
+  constexpr bool TW_REG = (ENG::T * ENG::T == N);
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int q = threadIdx.x % Q;
+  // four-step engines keep the thread's twiddles in registers (no shared-memory table)
+  float2 twr[TW_REG ? P : 1];
+  if constexpr (TW_REG) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) twr[k] = __ldg(a.wtab + k * Q + q);
+  }
+  pass_body<N, KIND, false>(a, blockIdx.x, make_int4(0, 0, 0, 0), twr, smem);
+}
+
+// ------------------------------------------------------------------------------------------
+// Persistent chain kernel: the probe chains of a pass segment for all local tiles in one
+// cooperative launch.  Every grid step runs one pass index (all tiles in lockstep), the CTAs
+// sweep the (tile, line group) items statically, and a grid barrier separates the steps (the
+// next pass reads the transposed wavefield every CTA wrote).  The barrier's gpu-scope fence
+// also invalidates L1 (CCTL.IVALL), so V/AccBuf rows written by other SMs are never read stale.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire(bar) < target) {
+      __nanosleep(32);
+      if (globaltimer() - t0 > 20000000000ull) __trap();  // 20 s: never hang the device
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__host__ __device__ constexpr int chain_kind(int p, int S) {
+  return S == 1 ? (p == 0 ? K_FWD_FIRST_FFT : (p == 1 ? K_TURN : K_BWD_LAST_END))
+                : (p == 0 ? K_FWD_FIRST_PROP
+                          : (p < S - 1 ? K_FWD_MID
+                                       : (p == S - 1 ? K_FWD_LAST
+                                                     : (p == S ? K_TURN
+                                                               : (p == S + 1 ? K_BWD_LAST_PROP
+                                                                             : (p < 2 * S ? K_BWD_MID : K_BWD_END))))));
+}
+__host__ __device__ constexpr int chain_slice(int p, int S) { return p < S ? p : (p == S ? S : 2 * S - p); }
+
+template <int N>
+__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2) chain_kernel(const ChainArgs c) {
+  using ENG = typename EngOf<N>::type;
+  constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
+  constexpr bool TW_REG = (ENG::T * ENG::T == N);
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int q = threadIdx.x % Q;
+  float2 twr[TW_REG ? P : 1];
+  if constexpr (TW_REG) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) twr[k] = __ldg(c.t[0].wtab + k * Q + q);
+  } else {
+    for (int e = threadIdx.x; e < ENG::TW; e += L * Q) ((float2*)smem)[e] = c.t[0].wtab[e];
+  }
+  {  // H_1/N table (same offset for every pass kind)
+    float2* ht = (float2*)(smem + Smem<N, K_FWD_MID>::ht);
+    for (int e = threadIdx.x; e <= N / 2; e += L * Q) ht[e] = c.t[0].htab[e];
+  }
+  const int S = c.S, groups = N / L, items = c.ntiles * groups;
+  unsigned target = 0;
+  for (int j = 0; j < c.maxn; ++j) {
+    for (int pp = 0; pp < 2 * S + 1; ++pp) {
+      const int kind = chain_kind(pp, S), sl = chain_slice(pp, S);
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int tl = it / groups, grp = it - tl * groups;
+        if (j >= c.count[tl]) continue;  // block-uniform
+        PassArgs a = c.t[tl];
+        a.s = sl;
+        a.in = pp == 0 ? a.probe : c.wf[tl][pp & 1];
+        a.out = c.wf[tl][(pp + 1) & 1];
+        const int pi = c.first + j;
+        const int2 ctr = a.centers[pi];
+        const int4 pd = make_int4(pi, ctr.x - N / 2, ctr.y - N / 2, 0);
+        switch (kind) {
+          case K_FWD_FIRST_PROP: pass_body<N, K_FWD_FIRST_PROP, true>(a, grp, pd, twr, smem); break;
+          case K_FWD_FIRST_FFT: pass_body<N, K_FWD_FIRST_FFT, true>(a, grp, pd, twr, smem); break;
+          case K_FWD_MID: pass_body<N, K_FWD_MID, true>(a, grp, pd, twr, smem); break;
+          case K_FWD_LAST: pass_body<N, K_FWD_LAST, true>(a, grp, pd, twr, smem); break;
+          case K_TURN: pass_body<N, K_TURN, true>(a, grp, pd, twr, smem); break;
+          case K_BWD_LAST_PROP: pass_body<N, K_BWD_LAST_PROP, true>(a, grp, pd, twr, smem); break;
+          case K_BWD_LAST_END: pass_body<N, K_BWD_LAST_END, true>(a, grp, pd, twr, smem); break;
+          case K_BWD_MID: pass_body<N, K_BWD_MID, true>(a, grp, pd, twr, smem); break;
+          default: pass_body<N, K_BWD_END, true>(a, grp, pd, twr, smem); break;
+        }
+      }
+      target += gridDim.x;
+      grid_barrier(c.bar, target);
+    }
+  }
+}
+
+template <int N>
+static size_t chain_smem() {
+  size_t m = 0;
+  const size_t v[] = {Smem<N, K_FWD_FIRST_PROP>::total, Smem<N, K_FWD_FIRST_FFT>::total, Smem<N, K_FWD_MID>::total,
+                      Smem<N, K_FWD_LAST>::total,       Smem<N, K_TURN>::total,          Smem<N, K_BWD_LAST_PROP>::total,
+                      Smem<N, K_BWD_LAST_END>::total,   Smem<N, K_BWD_MID>::total,       Smem<N, K_BWD_END>::total};
+  for (size_t x : v) m = x > m ? x : m;
+  return m;
+}
+
+template <int N>
+static cudaError_t launch_chain_n(const ChainArgs& c, cudaStream_t stream) {
+  auto kern = chain_kernel<N>;
+  const size_t smem = chain_smem<N>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int threads = LINES_PER_CTA * EngThreads<N>::v;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per < 1) return cudaErrorCooperativeLaunchTooLarge;
+  int grid = per * sms;
+  const int items = c.ntiles * (N / LINES_PER_CTA);
+  if (grid > items) grid = items;
+  void* args[] = {(void*)&c};
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, stream);
+}
+
+cudaError_t launch_chain(int n, const ChainArgs& c, cudaStream_t stream) {
+  switch (n) {
+    case 64: return launch_chain_n<64>(c, stream);
+    case 256: return launch_chain_n<256>(c, stream);
+    case 1024: return launch_chain_n<1024>(c, stream);
+    default: return cudaErrorInvalidValue;
   }
 }
 
