@@ -1,0 +1,71 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (the config's
+tile grid as virtual tiles on one GPU, halo N/2, CUDA-graph + PDL chains, occupancy-selected
+kernels), on sampled outputs the float64 oracle computes one by one: the AccBuf / V update of one
+probe of one tile after a real forward_grad, and the per-probe gradient and loss.
+
+Tolerance: max(1e-5, 2 x fp32 floor) rel L2 (the floor = the same oracle run in float32,
+SURVEY §8(c.5)); a few minutes of oracle time per config."""
+import numpy as np
+import pytest
+
+from oracle import ptycho_oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a - b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+@pytest.mark.parametrize("name,tile,local", [("lt_small", 5, 200), ("appp", 3, 500), ("lt_small", 0, 0)])
+def test_fullsize_sampled_update(name, tile, local):
+    from paper_2205_06327_b200.ptycho import Ptycho
+    c = synth.CONFIGS[name]
+    n, s, h, w = c.n, c.slices, c.height, c.width
+    rows, cols = c.grid
+    probe = synth.probe(n, c.defocus_nm)
+    vt = synth.volume(0, s, h, w)
+    v0 = (0.5 * vt).astype(np.float32)
+    centers = synth.scan_centers(h, w, c.scan_ny, c.scan_nx)
+    tiles = O.tile_geometry(h, w, rows, cols, n // 2)
+    asg = O.assign_probes(centers, tiles)
+    gid = asg[tile][local]
+    ext = tiles[tile]["ext"]
+    center = tuple(int(v) for v in centers[gid])
+
+    amp = O.farfield_magnitude(probe, O.window(vt.astype(np.float64), (0, 0, h, w), center, n), c.sigma, c.prop_c)
+    vwin = O.window(v0.astype(np.float64), (0, 0, h, w), center, n)
+    g_ref, f_ref = O.probe_grad(probe, vwin, amp, c.sigma, c.prop_c)
+    g32, _ = O.probe_grad(probe, vwin, amp, c.sigma, c.prop_c, dtype=np.float32)
+    floor = rel(g32, g_ref)
+    tol = max(1e-5, 2 * floor)
+
+    alpha = 0.5
+    p = Ptycho(n, s, h, w, c.sigma, c.prop_c, alpha=alpha)
+    p.set_tiles(rows, cols, n // 2)
+    p.set_scan(centers)
+    p.allocate_workspace()
+    p.set_probe(probe.astype(np.complex64))
+    first_local = sum(len(a) for a in asg[:tile]) + local  # local order: tiles ascending
+    p.load_measurements(amp[None].astype(np.float32), first_local=first_local)
+    p.set_volume(v0)
+
+    g, f = p.debug_probe_grad(tile, local)
+    e_grad = rel(g, g_ref)
+
+    # the real hot path: every tile processes its local probe `local` (graphs + PDL)
+    p.forward_grad(local, 1)
+    acc = p.debug_read_tile(tile, 1)
+    vk = p.debug_read_tile(tile, 0)
+    mask = O.window_mask(ext, center, n)
+    full_g = np.zeros((s, ext[2] - ext[0], ext[3] - ext[1]))
+    O._scatter(full_g, ext, center, n, g_ref, mask, 1.0)
+    e_acc = rel(acc, full_g)
+    v0k = v0[:, ext[0]:ext[2], ext[1]:ext[3]].astype(np.float64)
+    e_dv = rel((v0k - vk) / alpha, full_g)
+    print(f"{name} tile {tile} probe {local} (global {gid}): grad {e_grad:.2e}, AccBuf {e_acc:.2e}, "
+          f"dV/alpha {e_dv:.2e} (fp32 floor {floor:.2e}); loss rel {abs(f - f_ref) / f_ref:.2e}")
+    assert e_grad <= tol and e_acc <= tol and e_dv <= max(tol, 1e-4)
+    assert abs(f - f_ref) <= 1e-5 * f_ref
+    p.close()

@@ -269,3 +269,31 @@ def test_error_codes():
     with pytest.raises(PtychoError) as e:
         q.set_scan(np.array([[200, 5]], np.int32))
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("s", [1, 2])
+def test_degenerate_slices_and_empty_tile(s):
+    """S = 1 and 2 (the chain's special first/last passes) and a tile with no probes at all."""
+    n, h, w = 64, 140, 120
+    rng = np.random.default_rng(4)
+    probe = synth.probe(n, 8.0)
+    vt = rng.random((s, h, w)).astype(np.float32)
+    centers = synth.scan_centers(h // 2, w, 3, 4)  # only the upper half: tiles of the lower row are empty
+    d = dict(n=n, slices=s, height=h, width=w, sigma=0.3, prop_c=3.135)
+    amps = np.stack([O.farfield_magnitude(probe, O.window(vt.astype(np.float64), (0, 0, h, w), tuple(cc), n),
+                                          d["sigma"], d["prop_c"]) for cc in centers]).astype(np.float32)
+    v0 = (0.5 * vt).astype(np.float32)
+    ref, losses, _, _ = O.reconstruct(v0.astype(np.float64), probe, amps.astype(np.float64), centers, d, 2, 2,
+                                      n // 2, 2, alpha=1.0, period=2)
+    p = make(d, rows=2, cols=2, alpha=1.0, period=2)
+    p.set_scan(centers)
+    assert p.tile_probe_count(2) == 0 and p.tile_probe_count(3) == 0
+    p.allocate_workspace()
+    p.set_probe(probe.astype(np.complex64))
+    p.load_measurements(amps[p.local_probes()])
+    p.set_volume(v0)
+    got = [p.iterate(want_loss=True) for _ in range(2)]
+    out = p.stitch()
+    assert rel(out, ref) <= 1e-4 and rel(out - v0, ref - v0) <= 1e-3
+    for a, b in zip(got, losses):
+        assert abs(a - b) <= 1e-4 * b
