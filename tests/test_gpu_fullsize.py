@@ -18,7 +18,8 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a - b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
-@pytest.mark.parametrize("name,tile,local", [("lt_small", 5, 200), ("appp", 3, 500), ("lt_small", 0, 0)])
+@pytest.mark.parametrize("name,tile,local", [("lt_small", 5, 200), ("appp", 3, 500), ("lt_small", 0, 0),
+                                             ("lt_large", 6, 1500)])
 def test_fullsize_sampled_update(name, tile, local):
     from paper_2205_06327_b200.ptycho import Ptycho
     c = synth.CONFIGS[name]
