@@ -135,6 +135,16 @@ ptycho_status ptycho_tile_probe_count(ptycho_ctx ctx, int32_t tile, int64_t* cou
 /* Rects of tile `tile`: ext = R_k, interior = the non-halo part (both may be NULL). */
 ptycho_status ptycho_tile_rect(ptycho_ctx ctx, int32_t tile, int32_t ext[4], int32_t interior[4]);
 
+/* Opt-in batched schedule (north_star item 3; the sequential per-probe update of Alg. 1 steps
+ * 5-8, is the default): within each pass segment a tile's probes are grouped into rounds
+ * -- round(i) = 1 + the largest round of an earlier probe whose window (clipped to R_k) overlaps
+ * window i -- and each round's probes (ascending) run side by side in batches of <= max_batch
+ * (1..64).  Every voxel sees the same ordered sequence of updates as in the sequential schedule,
+ * so V_k and AccBuf_k are bit-identical to it (the reported loss may differ in rounding: its
+ * partial sums are grouped per batch slot).  Costs max_batch x (stash + wavefields) of workspace.
+ * Call after set_scan and before set_workspace. */
+ptycho_status ptycho_set_schedule(ptycho_ctx ctx, int32_t batched, int32_t max_batch);
+
 /* Bytes of device workspace this rank needs (after set_tiles and set_scan). */
 ptycho_status ptycho_workspace_bytes(ptycho_ctx ctx, size_t* bytes);
 

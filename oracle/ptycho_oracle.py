@@ -348,8 +348,29 @@ def n_segments(assignment, period: int) -> int:
     return -(-nmax // t)
 
 
+def batch_order(seg, centers, ext, n, max_batch):
+    """Batched schedule (north_star item 3): the probes `seg` (ascending) regrouped into batches of
+    pairwise non-overlapping windows (clipped to R_k): round(i) = 1 + max round of an earlier
+    overlapping probe; each round (ascending) split into batches of max_batch.  Returns the probe
+    order the batches imply."""
+    rects, rounds = [], []
+    for i in seg:
+        cy, cx = int(centers[i][0]), int(centers[i][1])
+        r = (max(cy - n // 2, ext[0]), min(cy - n // 2 + n, ext[2]), max(cx - n // 2, ext[1]), min(cx - n // 2 + n, ext[3]))
+        k = 0
+        for rj, kj in zip(rects, rounds):
+            if rj[0] < r[1] and r[0] < rj[1] and rj[2] < r[3] and r[2] < rj[3]:
+                k = max(k, kj + 1)
+        rects.append(r)
+        rounds.append(k)
+    order = []
+    for k in range(max(rounds, default=-1) + 1):
+        order += [i for i, kk in zip(seg, rounds) if kk == k]
+    return order
+
+
 def reconstruct(v0, probe, amps, centers, cfg, rows, cols, halo, iterations, alpha,
-                alpha_acc=None, period=0, tau=TAU, on_segment=None):
+                alpha_acc=None, period=0, tau=TAU, on_segment=None, batch=0):
     """Run Alg. 1 literally.
 
     For each iteration, for each pass segment j, for each tile k (independent between passes):
@@ -375,7 +396,10 @@ def reconstruct(v0, probe, amps, centers, cfg, rows, cols, halo, iterations, alp
         total = 0.0
         for j in range(nseg):
             for k, t in enumerate(tiles):
-                for i in assignment[k][j * t_per:(j + 1) * t_per]:
+                seg = assignment[k][j * t_per:(j + 1) * t_per]
+                if batch:  # batched schedule: same per-voxel update order (batch_order)
+                    seg = batch_order(seg, centers, t["ext"], n, batch)
+                for i in seg:
                     cy, cx = int(centers[i][0]), int(centers[i][1])
                     vwin = window(vks[k], t["ext"], (cy, cx), n)
                     g, f = probe_grad(probe, vwin, amps[i], sigma, c, tau)

@@ -50,6 +50,11 @@ struct Tile {
   cudaEvent_t ev = nullptr;
   cudaGraphExec_t graph = nullptr;
   std::vector<cudaEvent_t> slab_ev;  // APPP slab pipelining (segment_pipelined)
+  // batched schedule
+  int* order = nullptr;                  // device: probe lists of the current batches
+  cudaGraphExec_t graph_b = nullptr;     // chain over `batch` slots, no cursor advance
+  int64_t bfirst = -1, bcount = -1;      // cached batches for local probes [bfirst, bfirst+bcount)
+  std::vector<std::vector<int>> batches;
 };
 
 constexpr size_t ALIGN = 256;
@@ -97,6 +102,8 @@ struct ptycho_ctx_s {
   bool use_pdl = true;
   int slab = 0;  // slices per APPP slab in ptycho_iterate (0 = passes after the whole segment)
   bool persist = false;  // run probe chains in the persistent cooperative chain kernel
+  bool batched = false;  // opt-in batched schedule (non-overlapping windows side by side)
+  int batch = 1;         // batch slots per tile
 };
 
 static thread_local std::string g_create_err;
@@ -184,6 +191,7 @@ extern "C" ptycho_status ptycho_destroy(ptycho_ctx ctx) {
   cudaSetDevice(ctx->device);
   for (auto& t : ctx->tiles) {
     if (t.graph) cudaGraphExecDestroy(t.graph);
+    if (t.graph_b) cudaGraphExecDestroy(t.graph_b);
     if (t.stream) cudaStreamDestroy(t.stream);
     if (t.ev) cudaEventDestroy(t.ev);
     for (cudaEvent_t e : t.slab_ev) cudaEventDestroy(e);
@@ -447,14 +455,16 @@ static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
     const size_t vol = (size_t)t.slice_stride * S;
     t.V = (float*)take(vol * sizeof(float));
     t.acc = (float*)take(vol * sizeof(float));
-    t.stash = (float2*)take(S * n2 * sizeof(float2));
-    t.wf[0] = (float2*)take(n2 * sizeof(float2));
-    t.wf[1] = (float2*)take(n2 * sizeof(float2));
+    const size_t B = (size_t)ctx->batch;
+    t.stash = (float2*)take(B * S * n2 * sizeof(float2));
+    t.wf[0] = (float2*)take(B * n2 * sizeof(float2));
+    t.wf[1] = (float2*)take(B * n2 * sizeof(float2));
+    t.order = (int*)take(std::max<size_t>(t.probes.size(), 1) * sizeof(int));
     t.amp = (float*)take(std::max<size_t>(t.probes.size(), 1) * n2 * sizeof(float));
     t.centers = (int2*)take(std::max<size_t>(t.probes.size(), 1) * sizeof(int2));
-    t.desc = (int4*)take(sizeof(int4));
+    t.desc = (int4*)take(B * sizeof(int4));
     t.done = (unsigned*)take(sizeof(unsigned));
-    t.loss_part = (double*)take((n / LINES_PER_CTA) * sizeof(double));
+    t.loss_part = (double*)take(B * (n / LINES_PER_CTA) * sizeof(double));
   }
   return off;
 }
@@ -497,9 +507,9 @@ extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_de
     for (size_t j = 0; j < t.probes.size(); ++j)
       hc[j] = make_int2(ctx->centers[2 * t.probes[j]], ctx->centers[2 * t.probes[j] + 1]);
     CK(cudaMemcpyAsync(t.centers, hc.data(), hc.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemsetAsync(t.desc, 0, sizeof(int4), ctx->stream));
+    CK(cudaMemsetAsync(t.desc, 0, ctx->batch * sizeof(int4), ctx->stream));
     CK(cudaMemsetAsync(t.done, 0, sizeof(unsigned), ctx->stream));
-    CK(cudaMemsetAsync(t.loss_part, 0, (n / LINES_PER_CTA) * sizeof(double), ctx->stream));
+    CK(cudaMemsetAsync(t.loss_part, 0, ctx->batch * (n / LINES_PER_CTA) * sizeof(double), ctx->stream));
     CK(cudaMemsetAsync(t.amp, 0, std::max<size_t>(t.probes.size(), 1) * n * n * sizeof(float), ctx->stream));
   }
   PASS(zero_tiles(ctx, true, true));
@@ -690,7 +700,7 @@ extern "C" ptycho_status ptycho_set_volume(ptycho_ctx ctx, const float* volume, 
 // ------------------------------------------------------------------------------------------
 // the per-probe pass chain (DESIGN.md §Pass schedule): 2S+1 kernels
 // ------------------------------------------------------------------------------------------
-enum ChainMode { CHAIN_GRAD = 0, CHAIN_SIMULATE, CHAIN_DEBUG_GRAD, CHAIN_DEBUG_EXIT };
+enum ChainMode { CHAIN_GRAD = 0, CHAIN_SIMULATE, CHAIN_DEBUG_GRAD, CHAIN_DEBUG_EXIT, CHAIN_BATCH };
 
 static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   PassArgs a{};
@@ -719,6 +729,9 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   a.thr = (float)(ctx->cfg.tau * ctx->probe_norm / ctx->cfg.n);
   // >= 4 tile chains share the GPU: prefer the forward-pass build with room for more CTAs
   a.high_occupancy = ctx->local.size() >= 4 ? 1 : 0;
+  a.batch = 1;  // the batched graph overrides (set_schedule)
+  a.stash_slot = (long long)ctx->cfg.slices * ctx->cfg.n * ctx->cfg.n;
+  a.wf_slot = (long long)ctx->cfg.n * ctx->cfg.n;
   return a;
 }
 
@@ -739,6 +752,7 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
     b.in = t.wf[pass & 1];
     b.out = t.wf[(pass + 1) & 1];
     b.advance = (last && (mode == CHAIN_GRAD || mode == CHAIN_SIMULATE)) ? 1 : 0;
+    if (mode == CHAIN_BATCH) b.batch = ctx->batch;  // descriptors set per batch by the host
     if (mode == CHAIN_DEBUG_GRAD) b.gexport = ctx->debug;
     if (mode == CHAIN_DEBUG_EXIT) {
       b.natural_out = (float2*)ctx->debug;
@@ -783,12 +797,13 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
 
 static int chain_len(int S) { return 2 * S + 1; }
 
-static ptycho_status ensure_graph(ptycho_ctx ctx, Tile& t) {
-  if (t.graph || !ctx->use_graph) return PTYCHO_OK;
+static ptycho_status ensure_graph(ptycho_ctx ctx, Tile& t, ChainMode mode = CHAIN_GRAD) {
+  cudaGraphExec_t* slot = mode == CHAIN_BATCH ? &t.graph_b : &t.graph;
+  if (*slot || !ctx->use_graph) return PTYCHO_OK;
   cudaGraph_t g = nullptr;
   CK(cudaStreamBeginCapture(t.stream, cudaStreamCaptureModeThreadLocal));
   const long long before = ctx->launches;
-  ptycho_status st = enqueue_chain(ctx, t, CHAIN_GRAD, t.stream);
+  ptycho_status st = enqueue_chain(ctx, t, mode, t.stream);
   cudaError_t e = cudaStreamEndCapture(t.stream, &g);
   ctx->launches = before;  // captured, not launched
   if (st != PTYCHO_OK) {
@@ -796,11 +811,47 @@ static ptycho_status ensure_graph(ptycho_ctx ctx, Tile& t) {
     return st;
   }
   CK(e);
-  e = cudaGraphInstantiateWithFlags(&t.graph, g, 0);
+  e = cudaGraphInstantiateWithFlags(slot, g, 0);
   cudaGraphDestroy(g);
   CK(e);
   return PTYCHO_OK;
 }
+
+// Batched schedule (north_star item 3): local probes [first, first+m) of tile t
+// in batches of pairwise non-overlapping windows.  Round of probe i = 1 + the largest round of an
+// earlier probe whose window (clipped to R_k) meets it; a round's probes, ascending, are split
+// into batches of at most `batch`.  Every voxel then sees the updates of the probes covering it in
+// ascending index order, and every probe reads V after all earlier overlapping probes -> results
+// bit-identical to the sequential schedule (V, AccBuf).
+static void make_batches(ptycho_ctx ctx, Tile& t, int64_t first, int64_t m) {
+  if (t.bfirst == first && t.bcount == m) return;
+  const int n = ctx->cfg.n;
+  std::vector<int> y0(m), y1(m), x0(m), x1(m), round(m, 0);
+  int nround = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t g = t.probes[first + i];
+    const int cy = ctx->centers[2 * g], cx = ctx->centers[2 * g + 1];
+    y0[i] = std::max(cy - n / 2, t.ey0);
+    y1[i] = std::min(cy - n / 2 + n, t.ey1);
+    x0[i] = std::max(cx - n / 2, t.ex0);
+    x1[i] = std::min(cx - n / 2 + n, t.ex1);
+    int r = 0;
+    for (int64_t j = 0; j < i; ++j)
+      if (round[j] >= r && y0[j] < y1[i] && y0[i] < y1[j] && x0[j] < x1[i] && x0[i] < x1[j]) r = round[j] + 1;
+    round[i] = r;
+    nround = std::max(nround, r + 1);
+  }
+  t.batches.clear();
+  std::vector<std::vector<int>> byr(nround);
+  for (int64_t i = 0; i < m; ++i) byr[round[i]].push_back((int)(first + i));
+  for (auto& r : byr)
+    for (size_t o = 0; o < r.size(); o += ctx->batch)
+      t.batches.emplace_back(r.begin() + o, r.begin() + std::min(r.size(), o + (size_t)ctx->batch));
+  t.bfirst = first;
+  t.bcount = m;
+}
+
+static ptycho_status run_batched(ptycho_ctx ctx, int64_t first, int64_t count);
 
 static ptycho_status set_cursor(ptycho_ctx ctx, Tile& t, int v, cudaStream_t st) {
   CK(launch_set_desc(t.desc, t.centers, v, (int)t.probes.size(), ctx->cfg.n, st));
@@ -831,7 +882,7 @@ static ptycho_status need_run(ptycho_ctx ctx) {
 
 static ptycho_status sum_loss(ptycho_ctx ctx, double* out_host) {
   // fixed-order sum: per tile (deterministic kernel), then tiles in increasing index on the host
-  const int parts = ctx->cfg.n / LINES_PER_CTA;
+  const int parts = ctx->batch * (ctx->cfg.n / LINES_PER_CTA);
   int j = 0;
   for (int k : ctx->local) {
     CK(launch_sum_double(ctx->tiles[k].loss_part, parts, ctx->dscratch + j, ctx->stream));
@@ -849,7 +900,8 @@ static ptycho_status sum_loss(ptycho_ctx ctx, double* out_host) {
 
 static ptycho_status zero_loss(ptycho_ctx ctx) {
   for (int k : ctx->local)
-    CK(cudaMemsetAsync(ctx->tiles[k].loss_part, 0, (ctx->cfg.n / LINES_PER_CTA) * sizeof(double), ctx->stream));
+    CK(cudaMemsetAsync(ctx->tiles[k].loss_part, 0, ctx->batch * (ctx->cfg.n / LINES_PER_CTA) * sizeof(double),
+                       ctx->stream));
   return PTYCHO_OK;
 }
 
@@ -883,6 +935,7 @@ static ptycho_status run_chain_kernel(ptycho_ctx ctx, int64_t first, const std::
 }
 
 static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, ChainMode mode) {
+  if (mode == CHAIN_GRAD && ctx->batched) return run_batched(ctx, first, count);
   if (mode == CHAIN_GRAD && ctx->persist) {
     std::vector<int64_t> cnt(ctx->tiles.size(), 0);
     for (int k : ctx->local)
@@ -913,6 +966,49 @@ static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, Ch
       }
     }
   return join_tiles(ctx);
+}
+
+static ptycho_status run_batched(ptycho_ctx ctx, int64_t first, int64_t count) {
+  PASS(fork_tiles(ctx));
+  size_t maxb = 0;
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const int64_t m = std::max<int64_t>(0, std::min<int64_t>(first + count, (int64_t)t.probes.size()) - first);
+    make_batches(ctx, t, first, m);
+    std::vector<int> flat;
+    for (auto& b : t.batches) flat.insert(flat.end(), b.begin(), b.end());
+    if (!flat.empty())
+      CK(cudaMemcpyAsync(t.order, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice, t.stream));
+    PASS(ensure_graph(ctx, t, CHAIN_BATCH));
+    maxb = std::max(maxb, t.batches.size());
+  }
+  std::vector<size_t> off(ctx->tiles.size(), 0);
+  for (size_t j = 0; j < maxb; ++j)
+    for (int k : ctx->local) {
+      Tile& t = ctx->tiles[k];
+      if (j >= t.batches.size()) continue;
+      const int cnt = (int)t.batches[j].size();
+      CK(launch_set_batch(t.desc, t.centers, t.order + off[k], cnt, ctx->batch, ctx->cfg.n, t.stream));
+      ++ctx->launches;
+      off[k] += cnt;
+      if (t.graph_b) {
+        CK(cudaGraphLaunch(t.graph_b, t.stream));
+        ctx->launches += chain_len(ctx->cfg.slices);
+      } else {
+        PASS(enqueue_chain(ctx, t, CHAIN_BATCH, t.stream));
+      }
+    }
+  return join_tiles(ctx);
+}
+
+extern "C" ptycho_status ptycho_set_schedule(ptycho_ctx ctx, int32_t batched, int32_t max_batch) {
+  if (!ctx) return PTYCHO_EARG;
+  if (!ctx->tiles_set || !ctx->scan_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles and set_scan first");
+  if (ctx->ws_set) return fail(ctx, PTYCHO_ESTATE, "set_schedule must precede set_workspace");
+  if (batched && (max_batch < 1 || max_batch > 64)) return fail(ctx, PTYCHO_EARG, "max_batch %d not in [1, 64]", max_batch);
+  ctx->batched = batched != 0;
+  ctx->batch = batched ? max_batch : 1;
+  return PTYCHO_OK;
 }
 
 extern "C" ptycho_status ptycho_forward_grad(ptycho_ctx ctx, int64_t first, int64_t count, double* loss_out) {
@@ -1018,6 +1114,11 @@ extern "C" ptycho_status ptycho_step(ptycho_ctx ctx) {
 // the passes and the accumulated step of a slab start as soon as every local tile reached it,
 // overlapping the backward passes of the lower slices.
 static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t count) {
+  if (ctx->batched) {  // batches end with whole batches: passes after the segment
+    PASS(run_probes(ctx, first, count, CHAIN_GRAD));
+    PASS(appp_range(ctx, 0, ctx->cfg.slices));
+    return step_range(ctx, 0, ctx->cfg.slices);
+  }
   const int S = ctx->cfg.slices, slab = ctx->slab, nslab = (S + slab - 1) / slab;
   int64_t maxn = 0;
   std::vector<int64_t> m(ctx->tiles.size(), 0);

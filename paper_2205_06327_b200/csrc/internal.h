@@ -38,6 +38,9 @@ struct PassArgs {
   int n_probes;             // probes of this tile (desc stops at the last one)
   int natural_transposed;   // debug store: lines are columns (1) or rows (0)
   int high_occupancy;       // forward passes built for 3 CTAs/SM (many concurrent tile chains)
+  int batch;                // probes processed side by side (batched schedule; 1 = sequential)
+  long long stash_slot;     // float2 between the stashes of consecutive batch slots
+  long long wf_slot;        // float2 between the wavefields of consecutive batch slots
 };
 
 enum PassKind : int {
@@ -85,6 +88,9 @@ cudaError_t launch_amp_load(float* dst, const float* src, int count, int n, int 
 // twiddle table of the FFT engine for window n (layout private to kernels.cu)
 size_t twiddle_table_size(int n);
 void fill_twiddles(int n, float2* tw);
+// desc[b] = probe list[b] for b < cnt, inactive (-1) for cnt <= b < batch
+cudaError_t launch_set_batch(int4* desc, const int2* centers, const int* list, int cnt, int batch, int n,
+                             cudaStream_t stream);
 // *desc = probe v of the tile (v clamped to [0, nk))
 cudaError_t launch_set_desc(int4* desc, const int2* centers, int v, int nk, int n, cudaStream_t stream);
 cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t stream);

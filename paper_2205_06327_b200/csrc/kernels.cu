@@ -477,6 +477,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     griddep_launch();
     pd = *a.desc;
   }
+  if (pd.x < 0) return;  // inactive batch slot (CTA-uniform; no barrier has been passed)
   const int i = pd.x, wy0 = pd.y, wx0 = pd.z;
   const int ax = a.s & 1;
   LineLoc LL = line_loc(a, ax, line, wy0, wx0);
@@ -729,7 +730,21 @@ pass_kernel(const PassArgs a) {
 #pragma unroll
     for (int k = 0; k < P; ++k) twr[k] = __ldg(a.wtab + k * Q + q);
   }
-  pass_body<N, KIND, false>(a, blockIdx.x, make_int4(0, 0, 0, 0), twr, smem);
+  // batched schedule: CTA block b of N/L lines serves batch slot b (its own stash, wavefields,
+  // probe descriptor and loss partials)
+  constexpr int groups = N / LINES_PER_CTA;
+  const int b = blockIdx.x / groups, grp = blockIdx.x - b * groups;
+  if (b == 0) {
+    pass_body<N, KIND, false>(a, grp, make_int4(0, 0, 0, 0), twr, smem);
+  } else {
+    PassArgs ab = a;
+    ab.stash += b * a.stash_slot;
+    ab.in += b * a.wf_slot;
+    ab.out += b * a.wf_slot;
+    ab.desc += b;
+    ab.loss_part += b * groups;
+    pass_body<N, KIND, false>(ab, grp, make_int4(0, 0, 0, 0), twr, smem);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -877,7 +892,7 @@ static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) 
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(N / LINES_PER_CTA);
+  cfg.gridDim = dim3((N / LINES_PER_CTA) * (a.batch > 1 ? a.batch : 1));
   cfg.blockDim = dim3(LINES_PER_CTA * EngOf<N>::type::T);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -1043,6 +1058,24 @@ cudaError_t launch_amp_load(float* dst, const float* src, int count, int n, int 
     amp_load_kernel<<<dim3(n, nc), 256, 0, stream>>>(dst + (long long)c0 * n * n, src + (long long)c0 * n * n, n,
                                                      shift, intensity, transpose);
   }
+  return cudaGetLastError();
+}
+
+__global__ void set_batch_kernel(int4* desc, const int2* centers, const int* list, int cnt, int batch, int n) {
+  const int b = threadIdx.x;
+  if (b >= batch) return;
+  if (b < cnt) {
+    const int v = list[b];
+    const int2 c = centers[v];
+    desc[b] = make_int4(v, c.x - n / 2, c.y - n / 2, 0);
+  } else {
+    desc[b] = make_int4(-1, 0, 0, 0);
+  }
+}
+
+cudaError_t launch_set_batch(int4* desc, const int2* centers, const int* list, int cnt, int batch, int n,
+                             cudaStream_t stream) {
+  set_batch_kernel<<<1, ((batch + 31) / 32) * 32, 0, stream>>>(desc, centers, list, cnt, batch, n);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,7 @@ _SIGS = {
     "ptycho_local_probes": [_P, _P, _c.POINTER(_c.c_int64)],
     "ptycho_tile_probe_count": [_P, _c.c_int32, _c.POINTER(_c.c_int64)],
     "ptycho_tile_rect": [_P, _c.c_int32, _P, _P],
+    "ptycho_set_schedule": [_P, _c.c_int32, _c.c_int32],
     "ptycho_workspace_bytes": [_P, _c.POINTER(_c.c_size_t)],
     "ptycho_set_workspace": [_P, _P, _c.c_size_t],
     "ptycho_set_probe": [_P, _P, _c.c_int],
@@ -194,6 +195,9 @@ class Ptycho:
         inter = np.zeros(4, np.int32)
         self._ck(lib.ptycho_tile_rect(self.h, tile, ext.ctypes.data, inter.ctypes.data))
         return tuple(int(v) for v in ext), tuple(int(v) for v in inter)
+
+    def set_schedule(self, batched, max_batch=8):
+        self._ck(lib.ptycho_set_schedule(self.h, int(bool(batched)), max_batch))
 
     def workspace_bytes(self):
         b = ctypes.c_size_t()

@@ -297,3 +297,38 @@ def test_degenerate_slices_and_empty_tile(s):
     assert rel(out, ref) <= 1e-4 and rel(out - v0, ref - v0) <= 1e-3
     for a, b in zip(got, losses):
         assert abs(a - b) <= 1e-4 * b
+
+
+@pytest.mark.parametrize("grid,period,batch", [((1, 1), 0, 4), ((2, 3), 3, 2), ((2, 2), 0, 8)])
+def test_batched_schedule_bit_identical(grid, period, batch):
+    """opt-in batched schedule == sequential, bitwise (V, AccBuf); and vs the oracle running it."""
+    n, s, h, w = 64, 3, 220, 200
+    rng = np.random.default_rng(5)
+    probe = synth.probe(n, 8.0)
+    vt = rng.random((s, h, w)).astype(np.float32)
+    centers = synth.scan_centers(h, w, 7, 6)
+    d = dict(n=n, slices=s, height=h, width=w, sigma=0.3, prop_c=3.135)
+    amps = np.stack([O.farfield_magnitude(probe, O.window(vt.astype(np.float64), (0, 0, h, w), tuple(cc), n),
+                                          d["sigma"], d["prop_c"]) for cc in centers]).astype(np.float32)
+    v0 = (0.5 * vt).astype(np.float32)
+    outs, accs = [], []
+    for batched in (False, True):
+        p = make(d, rows=grid[0], cols=grid[1], alpha=1.0, period=period)
+        p.set_scan(centers)
+        if batched:
+            p.set_schedule(True, batch)
+        p.allocate_workspace()
+        p.set_probe(probe.astype(np.complex64))
+        p.load_measurements(amps[p.local_probes()])
+        p.set_volume(v0)
+        p.iterate()
+        outs.append(p.stitch())
+        p.forward_grad(0, 10 ** 6)  # AccBuf after one more sweep (no passes)
+        accs.append([p.debug_read_tile(k, 1) for k in range(grid[0] * grid[1])])
+        p.close()
+    assert np.array_equal(outs[0], outs[1])
+    for a, b in zip(*accs):
+        assert np.array_equal(a, b)
+    ref, _, _, _ = O.reconstruct(v0.astype(np.float64), probe, amps.astype(np.float64), centers, d, grid[0], grid[1],
+                                 n // 2, 1, alpha=1.0, period=period, batch=batch)
+    assert rel(outs[1], ref) <= 1e-4 and rel(outs[1] - v0, ref - v0) <= 1e-3

@@ -401,3 +401,13 @@ def test_segments():
     assert O.n_segments(asg, 3) == 4
     assert O.n_segments(asg, 10) == 1
     assert O.n_segments([[], []], 0) == 0
+
+
+def test_batched_schedule_is_exactly_sequential():
+    # windows of one batch are disjoint: every voxel sees the same update sequence (float64 exact)
+    p, vt, centers, cfg, amps = _tiny_problem(n=16, s=2, h=60, w=60, ny=6, nx=6)
+    a, _, _, _ = O.reconstruct(0.5 * vt, p, amps, centers, cfg, 2, 2, 8, 2, alpha=1.0, period=5)
+    b, _, _, _ = O.reconstruct(0.5 * vt, p, amps, centers, cfg, 2, 2, 8, 2, alpha=1.0, period=5, batch=3)
+    assert np.array_equal(a, b)
+    order = O.batch_order(list(range(36)), centers, (0, 0, 60, 60), 16, 3)
+    assert sorted(order) == list(range(36)) and order != list(range(36))
