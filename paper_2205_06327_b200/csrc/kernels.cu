@@ -556,6 +556,24 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       // phi_s = exp(i sigma V_s[win ^ R_k]) psi_s  (t = 1 outside R_k, reading #12); stash phi_s
       cp_async_wait_all();
       float2* stp = a.stash + (size_t)a.s * N * N + (size_t)line * N + q;
+#ifndef PTYCHO_UNROLLED_STEPS
+      float2* xs = ex + q;  // rolled through the idle exchange buffer (instruction-cache footprint)
+#pragma unroll
+      for (int k = 0; k < P; ++k) xs[Q * k] = x[k];
+#pragma unroll 2
+      for (int k = 0; k < P; ++k) {
+        const float v = pv[q + Q * k];
+        float sn, cs;
+        sincos_t(a.sigma * v, &sn, &cs);
+        float2 y = xs[Q * k];
+        if (PL.transmit_cp) y.y = -y.y;
+        const float2 phi = cmul(y, make_float2(cs, sn));
+        xs[Q * k] = phi;
+        stp[Q * k] = phi;
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k) x[k] = xs[Q * k];
+#else
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         const float v = pv[q + Q * k];
@@ -566,6 +584,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         x[k] = cmul(y, make_float2(cs, sn));
         stp[Q * k] = x[k];
       }
+#endif
     } else if (has_step(PL, S_RESID) && st == S_RESID) {
       // X = raw 2-D DFT (N x true F phi_{S-1}); |Psi| = |X|/N (App. A: |H| = 1)
       cp_async_wait_all();
@@ -599,6 +618,34 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       const float two_sigma = 2.0f * a.sigma;
       const bool exporting = a.gexport != nullptr;  // debug: write g instead of updating
       const int lim = LL.ok ? LL.plim : 0;
+#ifndef PTYCHO_UNROLLED_STEPS
+      // Rolled over the line through the (idle) exchange buffer: the unrolled body was ~13 KB of
+      // SASS, and the pass loop (transform + steps) then overflowed the 32 KB instruction cache.
+      // Each thread only touches its own positions, so no synchronisation is needed.
+      float2* xs = ex;
+#pragma unroll
+      for (int k = 0; k < P; ++k) xs[ENG::idx(dist, q, k)] = x[k];
+#pragma unroll 2
+      for (int k = 0; k < P; ++k) {
+        const int j = ENG::idx(dist, q, k);
+        const int p = LL.pos0 + j;
+        const float2 ph = pst[j];
+        const float2 y = xs[j];
+        const float2 chi = make_float2(y.x, -y.y);
+        const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
+        const float v = pv[j];
+        if (!exporting && (unsigned)p < (unsigned)lim) {
+          arow[p] = pacc[j] + g;
+          vrow[p] = v - a.alpha * g;
+        }
+        pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
+        float sn, cs;
+        sincos_t(a.sigma * v, &sn, &cs);
+        xs[j] = cmulc(chi, make_float2(cs, sn));
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k) x[k] = xs[ENG::idx(dist, q, k)];
+#else
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         if ((k & 7) == 0) asm volatile("" ::: "memory");
@@ -617,6 +664,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         sincos_t(a.sigma * v, &sn, &cs);
         x[k] = cmulc(chi, make_float2(cs, sn));
       }
+#endif
       if (exporting) {
         ENG::sync_line(bid);
         float* o = a.gexport + (size_t)a.s * N * N;
