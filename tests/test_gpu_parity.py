@@ -332,3 +332,37 @@ def test_batched_schedule_bit_identical(grid, period, batch):
     ref, _, _, _ = O.reconstruct(v0.astype(np.float64), probe, amps.astype(np.float64), centers, d, grid[0], grid[1],
                                  n // 2, 1, alpha=1.0, period=period, batch=batch)
     assert rel(outs[1], ref) <= 1e-4 and rel(outs[1] - v0, ref - v0) <= 1e-3
+
+
+def test_measurement_layout_flags_and_round_trip():
+    """load_measurements: DC-centred intensities (reading #6: ifftshift once + sqrt at load) give
+    the same store as DC-at-origin amplitudes; read_measurements inverts the load (bit-exact)."""
+    from paper_2205_06327_b200.ptycho import PTYCHO_AMP_DC_CENTERED, PTYCHO_AMP_INTENSITY
+    for s in (3, 4):  # odd S stores the turnaround layout transposed
+        d = dict(n=64, slices=s, height=128, width=128, sigma=0.1, prop_c=3.1)
+        p = make(d)
+        p.set_scan(synth.scan_centers(128, 128, 2, 3))
+        p.allocate_workspace()
+        amp = synth.random_amplitudes(3, 6, 64)
+        p.load_measurements(amp)
+        assert np.array_equal(p.read_measurements(), amp)
+        inten = np.fft.fftshift(amp.astype(np.float64) ** 2, axes=(1, 2)).astype(np.float32)
+        p.load_measurements(inten, flags=PTYCHO_AMP_DC_CENTERED | PTYCHO_AMP_INTENSITY)
+        got = p.read_measurements()
+        assert np.abs(got - amp).max() <= 2e-7 * np.abs(amp).max()
+        p.close()
+
+
+def test_stitch_to_device_and_tile_rects():
+    import torch
+    d = dict(n=64, slices=3, height=150, width=131, sigma=0.1, prop_c=3.1)
+    p = make(d, rows=2, cols=3, halo=20)
+    p.set_scan(synth.scan_centers(150, 131, 3, 3))
+    p.allocate_workspace()
+    v = np.random.default_rng(6).random((3, 150, 131), dtype=np.float32)
+    p.set_volume(torch.from_numpy(v).cuda())
+    out = torch.zeros((3, 150, 131), dtype=torch.float32, device="cuda")
+    p.stitch(out)
+    assert np.array_equal(out.cpu().numpy(), v)
+    for k, t in enumerate(O.tile_geometry(150, 131, 2, 3, 20)):
+        assert p.tile_rect(k) == (t["ext"], t["interior"])
