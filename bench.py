@@ -88,6 +88,11 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------------------
+def workload_name(cfg):
+    return (f"{cfg.name}: {cfg.n}x{cfg.n}x{cfg.n_probes} measurements, "
+            f"{cfg.width}x{cfg.height}x{cfg.slices} object")
+
+
 def cpu_oracle_sample(cfg, probe, vt, centers, n_probes=1):
     """The float64 oracle, as it stands, on a bounded sample: the full forward + adjoint gradient
     of `n_probes` probes of the workload (N=1024, S=100).  Returns (probes/s, seconds, sample)."""
@@ -125,7 +130,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": value / PAPER_BEST_LT_SMALL,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "sample": "1 probe per step (bounded sample of the iteration)"},
+            "config": {"workload": workload_name(cfg), "sample": "1 probe per step (bounded sample of the iteration)"},
             "cpu_baseline": {"value": value, "unit": "probe-locations/s", "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "probe-locations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -165,6 +170,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="lt_small")
     ap.add_argument("--grid", default=None, help="tile grid RxC (default: the config's, 2x4)")
+    ap.add_argument("--halo", type=int, default=None,
+                    help="halo width (default N/2 = exact window; the paper's circle halo is 60)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -197,7 +204,8 @@ def main():
     alpha = 0.5
     stream = torch.cuda.Stream(local_rank)
     p = Ptycho(n, S, H, W, cfg.sigma, cfg.prop_c, alpha=alpha, device=local_rank, stream=stream.cuda_stream)
-    p.set_tiles(R, C, n // 2, owner, nid, rank, world)
+    halo = n // 2 if args.halo is None else args.halo
+    p.set_tiles(R, C, halo, owner, nid, rank, world)
     centers = synth.scan_centers(H, W, cfg.scan_ny, cfg.scan_nx)
     p.set_scan(centers)
     ws = p.allocate_workspace()
@@ -321,8 +329,8 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "sec_per_iteration": ms / 1e3,
                 "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": value / PAPER_BEST_LT_SMALL, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"{cfg.name}: {n}x{n}x{cfg.n_probes} measurements, {W}x{H}x{S} object",
-                           "grid": f"{R}x{C}", "halo": n // 2, "tiles_per_gpu": ntiles // world,
+                "config": {"workload": workload_name(cfg),
+                           "grid": f"{R}x{C}", "halo": halo, "tiles_per_gpu": ntiles // world,
                            "alpha": alpha, "pass_period": "once per iteration",
                            "l2": "inputs > L2 (V_k+AccBuf 8.9 GB, |y| 17.4 GB)",
                            "workspace_gb_per_gpu": ws / 1e9},
