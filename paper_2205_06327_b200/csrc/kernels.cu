@@ -477,7 +477,10 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     griddep_launch();
     pd = *a.desc;
   }
-  if (pd.x < 0) return;  // inactive batch slot (CTA-uniform; no barrier has been passed)
+  if (pd.x < 0) {  // inactive batch slot (CTA-uniform; no barrier has been passed)
+    cp_async_wait_all();  // the table copies must land before the CTA's shared memory is released
+    return;
+  }
   const int i = pd.x, wy0 = pd.y, wx0 = pd.z;
   const int ax = a.s & 1;
   LineLoc LL = line_loc(a, ax, line, wy0, wx0);
