@@ -178,6 +178,43 @@ def probe_grad(probe, vwin, amp, sigma, c, tau: float = TAU, dtype=np.float64):
     return g, f
 
 
+def probe_grad_recompute(probe, vwin, amp, sigma, c, tau: float = TAU, dtype=np.float64):
+    """The same gradient with phi_s recomputed backwards instead of stashed (SURVEY §8(f) #4,
+    derived from App. A: the propagator is unitary and |t_s| = 1, so
+      psi_{s+1} = F^-1 H F phi_s   =>   phi_s = F^-1 conj(H) F psi_{s+1},   psi_s = conj(t_s) phi_s).
+    Keeps only phi_{S-1} from the forward and runs, for s = S-1 .. 0, the chi recursion of
+    probe_grad next to the phi recursion
+      g_s = 2 sigma Im(chi conj(phi_s)) ; chi <- conj(t_s) chi ; phi <- conj(t_s) phi ;
+      chi <- F^-1 conj(H) F chi ; phi <- F^-1 conj(H) F phi.
+    In float64 it equals probe_grad to rounding; in float32 it gives the rounding floor of the
+    recomputation (the phi chain adds S-1 propagations).  Returns (g, f_i)."""
+    n = probe.shape[0]
+    cdt = np.complex64 if dtype == np.float32 else np.complex128
+    h = propagator(n, c).astype(cdt)
+    vwin = vwin.astype(dtype)
+    _, big_psi, phis = forward(probe, vwin, sigma, c, dtype)
+    phi = phis[-1]
+    mag = np.abs(big_psi)
+    resid = mag - amp.astype(dtype)
+    f = float(np.sum(resid ** 2))
+    thr = tau * math.sqrt(float(np.sum(np.abs(probe) ** 2))) / n
+    keep = mag > thr
+    chi_big = np.zeros_like(big_psi)
+    chi_big[keep] = resid[keep] * big_psi[keep] / mag[keep]
+    chi = ifft2(chi_big)
+    g = np.zeros(vwin.shape, dtype=dtype)
+    s_last = vwin.shape[0] - 1
+    for s in range(s_last, -1, -1):
+        chi = ifft2(np.conj(h) * fft2(chi))
+        if s < s_last:
+            phi = ifft2(np.conj(h) * fft2(phi))
+        g[s] = 2.0 * sigma * np.imag(chi * np.conj(phi))
+        t_conj = np.conj(np.exp(1j * dtype(sigma) * vwin[s])).astype(cdt)
+        chi = t_conj * chi
+        phi = t_conj * phi
+    return g, f
+
+
 def probe_grad_fd(probe, vwin, amp, sigma, c, eps: float = 1e-5) -> np.ndarray:
     """Central finite differences (f(V+e) - f(V-e)) / (2 eps) for every window voxel."""
     g = np.zeros(vwin.shape, dtype=np.float64)

@@ -152,6 +152,22 @@ def test_gradient_matches_central_differences(seed, n, s):
     assert rel(g, gfd) < 1e-5
 
 
+@pytest.mark.parametrize("seed,n,s", [(10, 8, 2), (11, 8, 3), (12, 12, 4)])
+def test_recomputed_gradient_matches_central_differences(seed, n, s):
+    # stash-free adjoint: phi_s rebuilt by inverse propagation must give the
+    # same d f / d V as finite differences of the forward model, and equal the stashed adjoint
+    rng = np.random.default_rng(seed)
+    p = crandn(rng, n, n)
+    p /= np.linalg.norm(p)
+    v = rng.random((s, n, n))
+    a = rng.random((n, n)) * 2 / n
+    sigma, c = 0.7, 1.3
+    g, f = O.probe_grad_recompute(p, v, a, sigma, c)
+    assert rel(g, O.probe_grad_fd(p, v, a, sigma, c, eps=1e-5)) < 1e-5
+    g0, f0 = O.probe_grad(p, v, a, sigma, c)
+    assert rel(g, g0) < 1e-12 and f == f0
+
+
 def test_gradient_stationary_at_generating_volume():
     n = 32
     rng = np.random.default_rng(6)
