@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--grid", default=None, help="tile grid RxC (default: the config's, 2x4)")
     ap.add_argument("--halo", type=int, default=None,
                     help="halo width (default N/2 = exact window; the paper's circle halo is 60)")
+    ap.add_argument("--stash-free", action="store_true",
+                    help="stash-free adjoint (PTYCHO_F_STASH_FREE): phi_s recomputed, 2-slice stash")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -182,7 +184,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2205_06327_b200.ptycho import Ptycho
+    from paper_2205_06327_b200.ptycho import Ptycho, PTYCHO_F_STASH_FREE
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -203,7 +205,8 @@ def main():
     n, S, H, W = cfg.n, cfg.slices, cfg.height, cfg.width
     alpha = 0.5
     stream = torch.cuda.Stream(local_rank)
-    p = Ptycho(n, S, H, W, cfg.sigma, cfg.prop_c, alpha=alpha, device=local_rank, stream=stream.cuda_stream)
+    p = Ptycho(n, S, H, W, cfg.sigma, cfg.prop_c, alpha=alpha, device=local_rank, stream=stream.cuda_stream,
+               flags=PTYCHO_F_STASH_FREE if args.stash_free else 0)
     halo = n // 2 if args.halo is None else args.halo
     p.set_tiles(R, C, halo, owner, nid, rank, world)
     centers = synth.scan_centers(H, W, cfg.scan_ny, cfg.scan_nx)
@@ -333,7 +336,8 @@ def main():
                            "grid": f"{R}x{C}", "halo": halo, "tiles_per_gpu": ntiles // world,
                            "alpha": alpha, "pass_period": "once per iteration",
                            "l2": "inputs > L2 (V_k+AccBuf 8.9 GB, |y| 17.4 GB)",
-                           "workspace_gb_per_gpu": ws / 1e9},
+                           "workspace_gb_per_gpu": ws / 1e9,
+                           "adjoint": "stash-free (phi recomputed)" if args.stash_free else "stash"},
                 "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
                 "e2e": e2e, "cpu_baseline": cpu, "loss_after": loss,
                 "paper_context": "GD small LT: 2310 probe-locations/s on 462 V100 (P:65-74)"}

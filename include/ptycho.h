@@ -53,6 +53,11 @@ typedef enum {
 
 /* ptycho_config.flags */
 #define PTYCHO_F_EXACT_WINDOW 1 /* require halo >= window reach (exact multi-tile == single tile) */
+#define PTYCHO_F_STASH_FREE 2   /* stash-free adjoint: keep phi_{S-1} only and     */
+                                /* recompute phi_s = P^H(conj(t_{s+1}) phi_{s+1}) during the backward */
+                                /* (P unitary, |t| = 1; App. A).  Stash 2 N^2 instead of S N^2        */
+                                /* complex64 per tile; S more passes per probe.  Same gradient up to  */
+                                /* fp32 rounding of the recomputation.                                */
 
 /* ptycho_load_measurements layout_flags */
 #define PTYCHO_AMP_DC_CENTERED 1 /* input has DC at (N/2,N/2): ifftshift once at load           */
@@ -217,8 +222,9 @@ ptycho_status ptycho_kernel_launches(ptycho_ctx ctx, int64_t* count);
 /* Measurement export (bench.py roofline): run the pass chain of local probes [first, first+count)
  * of local tile `tile` (real work: V_k and AccBuf_k are updated exactly as by forward_grad) with
  * direct launches bracketed by CUDA events on the tile's stream, and return per pass kind
- * (0..10, see PassKind in csrc/internal.h: 2 = forward middle pass, 8 = backward middle pass)
- * the summed kernel time in ms and the number of launches.  ms_out / launches_out: [11].
+ * (0..13, see PassKind in csrc/internal.h: 2 = forward middle pass, 8 = backward middle pass,
+ * 11..13 = stash-free recomputation passes) the summed kernel time in ms and the number of
+ * launches.  ms_out / launches_out: [14].
  * Synchronizes. */
 ptycho_status ptycho_profile_chain(ptycho_ctx ctx, int32_t tile, int64_t first, int64_t count, double* ms_out,
                                    int64_t* launches_out);

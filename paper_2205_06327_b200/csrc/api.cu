@@ -41,6 +41,7 @@ struct Tile {
   float* acc = nullptr;
   float2* stash = nullptr;
   float2* wf[2] = {nullptr, nullptr};
+  float2* wfr[2] = {nullptr, nullptr};  // phi-chain wavefields (PTYCHO_F_STASH_FREE)
   float* amp = nullptr;
   int2* centers = nullptr;
   int4* desc = nullptr;
@@ -58,6 +59,10 @@ struct Tile {
 };
 
 constexpr size_t ALIGN = 256;
+
+// phi_s stash slices per batch slot: all S, or the 2-slice ring of the stash-free adjoint
+static bool stash_free(const ptycho_config& c) { return (c.flags & PTYCHO_F_STASH_FREE) && c.slices > 1; }
+static size_t stash_slices(const ptycho_config& c) { return stash_free(c) ? 2 : (size_t)c.slices; }
 size_t align_up(size_t x, size_t a = ALIGN) { return (x + a - 1) / a * a; }
 
 }  // namespace
@@ -152,6 +157,8 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
     return fail(ctx, PTYCHO_EARG, "slices/height/width must be >= 1");
   if (cfg->pass_period < 0) return fail(ctx, PTYCHO_EARG, "pass_period T must be >= 0");
   if (!(cfg->tau >= 0.f)) return fail(ctx, PTYCHO_EARG, "tau must be >= 0");
+  if (cfg->flags & ~(PTYCHO_F_EXACT_WINDOW | PTYCHO_F_STASH_FREE))
+    return fail(ctx, PTYCHO_EARG, "unknown flags 0x%x", (unsigned)cfg->flags);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
     return fail(ctx, PTYCHO_ECUDA, "CUDA device %d not available", device);
@@ -165,6 +172,7 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   ctx->slab = std::max(1, (cfg->slices + 9) / 10);
   if (const char* e = getenv("PTYCHO_SLAB")) ctx->slab = std::max(0, atoi(e));
   if (const char* e = getenv("PTYCHO_PERSIST")) ctx->persist = atoi(e) != 0;
+  if (cfg->flags & PTYCHO_F_STASH_FREE) ctx->persist = false;  // the chain kernel keeps a full stash
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -456,9 +464,13 @@ static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
     t.V = (float*)take(vol * sizeof(float));
     t.acc = (float*)take(vol * sizeof(float));
     const size_t B = (size_t)ctx->batch;
-    t.stash = (float2*)take(B * S * n2 * sizeof(float2));
+    t.stash = (float2*)take(B * stash_slices(cfg) * n2 * sizeof(float2));
     t.wf[0] = (float2*)take(B * n2 * sizeof(float2));
     t.wf[1] = (float2*)take(B * n2 * sizeof(float2));
+    if (stash_free(cfg)) {
+      t.wfr[0] = (float2*)take(B * n2 * sizeof(float2));
+      t.wfr[1] = (float2*)take(B * n2 * sizeof(float2));
+    }
     t.order = (int*)take(std::max<size_t>(t.probes.size(), 1) * sizeof(int));
     t.amp = (float*)take(std::max<size_t>(t.probes.size(), 1) * n2 * sizeof(float));
     t.centers = (int2*)take(std::max<size_t>(t.probes.size(), 1) * sizeof(int2));
@@ -730,7 +742,8 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   // >= 4 tile chains share the GPU: prefer the forward-pass build with room for more CTAs
   a.high_occupancy = ctx->local.size() >= 4 ? 1 : 0;
   a.batch = 1;  // the batched graph overrides (set_schedule)
-  a.stash_slot = (long long)ctx->cfg.slices * ctx->cfg.n * ctx->cfg.n;
+  a.stash_slot = (long long)stash_slices(ctx->cfg) * ctx->cfg.n * ctx->cfg.n;
+  a.stash_store = 1;
   a.wf_slot = (long long)ctx->cfg.n * ctx->cfg.n;
   return a;
 }
@@ -745,12 +758,22 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
                                    int slab = 0) {
   const int S = ctx->cfg.slices, n = ctx->cfg.n;
   PassArgs a = base_args(ctx, t);
-  int pass = 0;
+  const bool ring = stash_free(ctx->cfg) && (mode == CHAIN_GRAD || mode == CHAIN_DEBUG_GRAD || mode == CHAIN_BATCH);
+  int pass = 0, rpass = 0;  // chi chain / phi chain (stash-free) ping-pong positions
   auto go = [&](PassKind kind, int s, bool last) -> ptycho_status {
     PassArgs b = a;
     b.s = s;
-    b.in = t.wf[pass & 1];
-    b.out = t.wf[(pass + 1) & 1];
+    const bool recon = kind == K_RECON_FIRST || kind == K_RECON_MID || kind == K_RECON_END;
+    b.stash_s = ring ? (s & 1) : s;
+    // stash-free: the forward keeps only phi_{S-1}; the phi chain recomputes the others
+    if (ring && (kind == K_FWD_FIRST_PROP || kind == K_FWD_MID)) b.stash_store = 0;
+    if (recon) {
+      b.in = t.wfr[rpass & 1];
+      b.out = t.wfr[(rpass + 1) & 1];
+    } else {
+      b.in = t.wf[pass & 1];
+      b.out = t.wf[(pass + 1) & 1];
+    }
     b.advance = (last && (mode == CHAIN_GRAD || mode == CHAIN_SIMULATE)) ? 1 : 0;
     if (mode == CHAIN_BATCH) b.batch = ctx->batch;  // descriptors set per batch by the host
     if (mode == CHAIN_DEBUG_GRAD) b.gexport = ctx->debug;
@@ -774,7 +797,8 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
     ++ctx->launches;
     const bool bwd = kind == K_BWD_LAST_PROP || kind == K_BWD_LAST_END || kind == K_BWD_MID || kind == K_BWD_END;
     if (slab_ev && bwd && s % slab == 0) CK(cudaEventRecord((*slab_ev)[s / slab], st));
-    ++pass;
+    if (recon) ++rpass;
+    else ++pass;
     return PTYCHO_OK;
   };
   // forward: pass s finishes psi_s's propagation along its axis, transmits, starts the next
@@ -790,12 +814,27 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
   if (mode == CHAIN_SIMULATE) return go(K_SIMULATE, S, true);
   PASS(go(K_TURN, S, false));
   if (S == 1) return go(K_BWD_LAST_END, 0, true);
+  if (!ring) {
+    PASS(go(K_BWD_LAST_PROP, S - 1, false));
+    for (int s = S - 2; s >= 1; --s) PASS(go(K_BWD_MID, s, false));
+    return go(K_BWD_END, 0, true);
+  }
+  // Stash-free adjoint: phi_{s-1} = P^H(conj(t_s) phi_s), from the stashed
+  // phi_{S-1}.  The phi chain runs one slice ahead of the gradient chain, so every stash-ring
+  // slot a gradient pass prefetches (before griddepcontrol.wait) was written >= 2 kernels earlier,
+  // and RECON(s) reads V_s before the gradient pass of slice s updates it.
+  auto recon = [&](int s) { return go(s == 0 ? K_RECON_END : K_RECON_MID, s, false); };
+  PASS(go(K_RECON_FIRST, S - 1, false));
+  PASS(recon(S - 2));
   PASS(go(K_BWD_LAST_PROP, S - 1, false));
-  for (int s = S - 2; s >= 1; --s) PASS(go(K_BWD_MID, s, false));
+  for (int s = S - 2; s >= 1; --s) {
+    PASS(recon(s - 1));
+    PASS(go(K_BWD_MID, s, false));
+  }
   return go(K_BWD_END, 0, true);
 }
 
-static int chain_len(int S) { return 2 * S + 1; }
+static int chain_len(int S, bool ring = false) { return 2 * S + 1 + (ring && S > 1 ? S : 0); }
 
 static ptycho_status ensure_graph(ptycho_ctx ctx, Tile& t, ChainMode mode = CHAIN_GRAD) {
   cudaGraphExec_t* slot = mode == CHAIN_BATCH ? &t.graph_b : &t.graph;
@@ -960,7 +999,7 @@ static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, Ch
       if (first + j >= nk) continue;
       if (mode == CHAIN_GRAD && t.graph) {
         CK(cudaGraphLaunch(t.graph, t.stream));
-        ctx->launches += chain_len(ctx->cfg.slices);
+        ctx->launches += chain_len(ctx->cfg.slices, stash_free(ctx->cfg));
       } else {
         PASS(enqueue_chain(ctx, t, mode, t.stream));
       }
@@ -993,7 +1032,7 @@ static ptycho_status run_batched(ptycho_ctx ctx, int64_t first, int64_t count) {
       off[k] += cnt;
       if (t.graph_b) {
         CK(cudaGraphLaunch(t.graph_b, t.stream));
-        ctx->launches += chain_len(ctx->cfg.slices);
+        ctx->launches += chain_len(ctx->cfg.slices, stash_free(ctx->cfg));
       } else {
         PASS(enqueue_chain(ctx, t, CHAIN_BATCH, t.stream));
       }
@@ -1148,7 +1187,7 @@ static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t co
       if (j >= m[k] || j < done[k]) continue;
       if (j < m[k] - 1 && t.graph) {
         CK(cudaGraphLaunch(t.graph, t.stream));
-        ctx->launches += chain_len(S);
+        ctx->launches += chain_len(S, stash_free(ctx->cfg));
       } else if (j < m[k] - 1) {
         PASS(enqueue_chain(ctx, t, CHAIN_GRAD, t.stream));
       } else {

@@ -18,7 +18,7 @@ struct PassArgs {
   long long slice_stride;   // floats per slice
   int pitch0, pitch1;       // row pitch of even slices ([eh][pitch0]) and odd slices ([ew][pitch1])
   int ey0, ex0, eh, ew;     // R_k in global coordinates
-  float2* stash;            // phi_s, [S][N][N] in layout L_{s&1}
+  float2* stash;            // phi_s, [S][N][N] in layout L_{s&1} (stash-free: a ring of 2 slices)
   const float2* in;         // wavefield in (line-major in this pass's layout)
   float2* out;              // wavefield out (written transposed)
   const float2* probe;      // p, [N][N] natural
@@ -33,7 +33,9 @@ struct PassArgs {
   float2* natural_out;      // debug: exit wave out [N][N] natural
   float sigma, alpha, thr;  // t = exp(i sigma V); per-probe step; |Psi| threshold (true scale)
   float sigma_pi;           // sigma / pi (t = sincospi(sigma_pi V), rounded from double)
-  int s;                    // slice index of this pass (TRANSMIT / GRAD)
+  int s;                    // slice index of this pass (TRANSMIT / GRAD / RECON)
+  int stash_s;              // stash slice of this pass (s, or s & 1 in the stash-free ring)
+  int stash_store;          // TRANSMIT writes phi_s to the stash (0: stash-free, s < S-1)
   int advance;              // last block advances *desc to the next probe when done
   int n_probes;             // probes of this tile (desc stops at the last one)
   int natural_transposed;   // debug store: lines are columns (1) or rows (0)
@@ -55,6 +57,11 @@ enum PassKind : int {
   K_BWD_MID,              // P^H ; grad/update ; P^H             ; store^T
   K_BWD_END,              // P^H ; grad/update                   (s = 0)
   K_EXIT_COMPLETE,        // P ; natural store (debug exit wave)
+  // stash-free adjoint (PTYCHO_F_STASH_FREE): phi_s = P^H(conj(t_{s+1}) phi_{s+1})
+  // is recomputed by a second adjoint chain running one slice ahead of the gradient chain.
+  K_RECON_FIRST,          // stash phi_{S-1} in; conj(t_{S-1}) ; P^H      ; store^T
+  K_RECON_MID,            // P^H ; phi_s -> stash ring ; conj(t_s) ; P^H ; store^T
+  K_RECON_END,            // P^H ; phi_0 -> stash ring
   K_COUNT
 };
 

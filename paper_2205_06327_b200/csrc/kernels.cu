@@ -332,6 +332,8 @@ enum Step : int {
   S_RESID,       // X = y ; loss ; chi = r X/(|X| N) ; y <- conj(chi)   (start of the 2-D inverse)
   S_SIMUL,       // |X| -> measurement store
   S_GRAD,        // chi_phi = conj(y) ; g ; AccBuf/V update ; y <- conj(t) chi_phi
+  S_RECON,       // phi_s = conj(y) -> stash ring ; y <- conj(t_s) phi_s   (stash-free adjoint)
+  S_RECON_T,     // y <- conj(t_s) y  (true phi_{S-1} from the stash)
 };
 
 // Per pass kind: steps before each F call, the step after the last F, and whether the stored
@@ -357,6 +359,11 @@ __host__ __device__ constexpr Plan plan_of(int kind) {
     case K_BWD_MID: return {4, {S_NONE, S_HC_ADJ, S_GRAD, S_HC_ADJ}, S_NONE, true, false};
     case K_BWD_END: return {2, {S_NONE, S_HC_ADJ, 0, 0}, S_GRAD, false, false};
     case K_EXIT_COMPLETE: return {2, {S_NONE, S_HC_FWD, 0, 0}, S_NONE, true, false};
+    // the phi chain mirrors the chi chain pass for pass (same P^H, same conj(t_s)): psi_s =
+    // conj(t_s) phi_s and phi_{s-1} = P^H psi_s (P unitary, |t_s| = 1; App. A)
+    case K_RECON_FIRST: return {2, {S_RECON_T, S_HC_ADJ, 0, 0}, S_NONE, true, false};
+    case K_RECON_MID: return {4, {S_NONE, S_HC_ADJ, S_RECON, S_HC_ADJ}, S_NONE, true, false};
+    case K_RECON_END: return {2, {S_NONE, S_HC_ADJ, 0, 0}, S_RECON, false, false};
     default: return {0, {0, 0, 0, 0}, 0, false, false};
   }
 }
@@ -372,9 +379,14 @@ __host__ __device__ constexpr bool kind_transmit(int k) {
 __host__ __device__ constexpr bool kind_grad(int k) {
   return k == K_BWD_LAST_PROP || k == K_BWD_LAST_END || k == K_BWD_MID || k == K_BWD_END;
 }
+__host__ __device__ constexpr bool kind_recon(int k) {
+  return k == K_RECON_FIRST || k == K_RECON_MID || k == K_RECON_END;
+}
 __host__ __device__ constexpr bool kind_first(int k) { return k == K_FWD_FIRST_PROP || k == K_FWD_FIRST_FFT; }
 __host__ __device__ constexpr int kind_store(int k) {
-  return k == K_SIMULATE || k == K_BWD_LAST_END || k == K_BWD_END ? 0 : (k == K_EXIT_COMPLETE ? 2 : 1);
+  return k == K_SIMULATE || k == K_BWD_LAST_END || k == K_BWD_END || k == K_RECON_END
+             ? 0
+             : (k == K_EXIT_COMPLETE ? 2 : 1);
 }
 
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -427,7 +439,8 @@ struct Smem {
   static constexpr size_t lines = ht + (N / 2 + 2) * 8;
   static constexpr size_t ex_b = (size_t)ENG::EX * 8;                // exchange buffer per line
   static constexpr size_t st_b = kind_grad(KIND) ? (size_t)N * 8 : 0;  // stash prefetch per line
-  static constexpr size_t v_b = (kind_transmit(KIND) || kind_grad(KIND) || KIND == K_TURN) ? (size_t)N * 4 : 0;
+  static constexpr size_t v_b =
+      (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND) || KIND == K_TURN) ? (size_t)N * 4 : 0;
   static constexpr size_t acc_b = kind_grad(KIND) ? (size_t)N * 4 : 0;  // AccBuf prefetch per line
   static constexpr size_t per_line = ex_b + st_b + v_b + acc_b;
   static constexpr size_t stage_b = (size_t)N * (L + 1) * 8;         // transposed-store staging
@@ -484,7 +497,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   const int i = pd.x, wy0 = pd.y, wx0 = pd.z;
   const int ax = a.s & 1;
   LineLoc LL = line_loc(a, ax, line, wy0, wx0);
-  if constexpr (kind_transmit(KIND) || kind_grad(KIND)) {
+  if constexpr (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND)) {
     const long long so = (long long)a.s * a.slice_stride + LL.row;
     const float* vrow = a.V + so;
     const float* arow = a.acc + so;
@@ -501,7 +514,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     }
   }
   if constexpr (kind_grad(KIND)) {
-    const float4* src = (const float4*)(a.stash + (size_t)a.s * N * N + (size_t)line * N);
+    const float4* src = (const float4*)(a.stash + (size_t)a.stash_s * N * N + (size_t)line * N);
     float4* dst = (float4*)pst;
 #pragma unroll 4
     for (int c = q; c < N / 2; c += Q) cp_async16(dst + c, src + c);
@@ -521,7 +534,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   } else if constexpr (!PERSIST) {
     griddep_wait();
     griddep_launch();
-    const float2* src = a.in + (size_t)line * N + q;
+    const float2* src = (KIND == K_RECON_FIRST ? a.stash + (size_t)a.stash_s * N * N : a.in) + (size_t)line * N + q;
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = src[Q * k];
   } else {
@@ -558,7 +571,8 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     } else if (has_step(PL, S_TRANSMIT) && st == S_TRANSMIT) {
       // phi_s = exp(i sigma V_s[win ^ R_k]) psi_s  (t = 1 outside R_k, reading #12); stash phi_s
       cp_async_wait_all();
-      float2* stp = a.stash + (size_t)a.s * N * N + (size_t)line * N + q;
+      float2* stp = a.stash + (size_t)a.stash_s * N * N + (size_t)line * N + q;
+      const bool keep = a.stash_store != 0;  // stash-free: only phi_{S-1} is kept
 #ifndef PTYCHO_UNROLLED_STEPS
       float2* xs = ex + q;  // rolled through the idle exchange buffer (instruction-cache footprint)
 #pragma unroll
@@ -572,7 +586,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         if (PL.transmit_cp) y.y = -y.y;
         const float2 phi = cmul(y, make_float2(cs, sn));
         xs[Q * k] = phi;
-        stp[Q * k] = phi;
+        if (keep) stp[Q * k] = phi;
       }
 #pragma unroll
       for (int k = 0; k < P; ++k) x[k] = xs[Q * k];
@@ -585,7 +599,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         float2 y = x[k];
         if (PL.transmit_cp) y.y = -y.y;
         x[k] = cmul(y, make_float2(cs, sn));
-        stp[Q * k] = x[k];
+        if (keep) stp[Q * k] = x[k];
       }
 #endif
     } else if (has_step(PL, S_RESID) && st == S_RESID) {
@@ -609,6 +623,31 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       float* am = a.amp + (size_t)i * N * N + (size_t)line * N;
 #pragma unroll
       for (int k = 0; k < P; ++k) am[ENG::idx(dist, q, k)] = sqrtf(x[k].x * x[k].x + x[k].y * x[k].y) * invn;
+    } else if ((has_step(PL, S_RECON) && st == S_RECON) || (has_step(PL, S_RECON_T) && st == S_RECON_T)) {
+      // stash-free adjoint: phi_s (conj pending after P^H, or true from the stash) -> stash ring
+      // slot; psi_s = conj(t_s) phi_s with t_s from the pre-update V (the gradient pass of slice
+      // s runs after this one).  Rolled through the idle exchange buffer like S_GRAD.
+      cp_async_wait_all();
+      ENG::sync_line(bid);
+      float2* stp = a.stash + (size_t)a.stash_s * N * N + (size_t)line * N;
+      const bool pending = (st == S_RECON);
+      float2* xs = ex;
+#pragma unroll
+      for (int k = 0; k < P; ++k) xs[ENG::idx(dist, q, k)] = x[k];
+#pragma unroll 2
+      for (int k = 0; k < P; ++k) {
+        const int j = ENG::idx(dist, q, k);
+        float2 phi = xs[j];
+        if (pending) {
+          phi.y = -phi.y;
+          stp[j] = phi;
+        }
+        float sn, cs;
+        sincos_t(a.sigma * pv[j], &sn, &cs);
+        xs[j] = cmulc(phi, make_float2(cs, sn));
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k) x[k] = xs[ENG::idx(dist, q, k)];
     } else if (has_step(PL, S_GRAD) && st == S_GRAD) {
       // chi_phi = conj(y).  g_s = 2 sigma Im(chi conj(phi_s)) (App. A); on win ^ R_k:
       // AccBuf += g (Alg. 1 step 7), V -= alpha g (step 8); chi <- conj(t_s) chi with t_s from
@@ -870,6 +909,8 @@ __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2) chain_ker
         if (j >= c.count[tl]) continue;  // block-uniform
         PassArgs a = c.t[tl];
         a.s = sl;
+        a.stash_s = sl;
+        a.stash_store = 1;
         a.in = pp == 0 ? a.probe : c.wf[tl][pp & 1];
         a.out = c.wf[tl][(pp + 1) & 1];
         const int pi = c.first + j;
@@ -969,6 +1010,9 @@ static cudaError_t launch_pass_nm(PassKind kind, const PassArgs& a, cudaStream_t
     case K_BWD_MID: return launch_one<N, K_BWD_MID, 2>(a, s, pdl);
     case K_BWD_END: return launch_one<N, K_BWD_END, 2>(a, s, pdl);
     case K_EXIT_COMPLETE: return launch_one<N, K_EXIT_COMPLETE, MINB>(a, s, pdl);
+    case K_RECON_FIRST: return launch_one<N, K_RECON_FIRST, MINB>(a, s, pdl);
+    case K_RECON_MID: return launch_one<N, K_RECON_MID, MINB>(a, s, pdl);
+    case K_RECON_END: return launch_one<N, K_RECON_END, MINB>(a, s, pdl);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PTYCHO_LIB", os.path.join(_HERE, "lib", "libptycho.so"))  # override: A/B builds
 
 PTYCHO_F_EXACT_WINDOW = 1
+PTYCHO_F_STASH_FREE = 2
 PTYCHO_AMP_DC_CENTERED = 1
 PTYCHO_AMP_INTENSITY = 2
 STATUS = {0: "OK", 1: "EARG", 2: "ESHAPE", 3: "ESTATE", 4: "EHALO", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
@@ -271,11 +272,12 @@ class Ptycho:
         return v.value
 
     PASS_KINDS = ["fwd_first_prop", "fwd_first_fft", "fwd_mid", "fwd_last", "turn", "simulate",
-                  "bwd_last_prop", "bwd_last_end", "bwd_mid", "bwd_end", "exit_complete"]
+                  "bwd_last_prop", "bwd_last_end", "bwd_mid", "bwd_end", "exit_complete",
+                  "recon_first", "recon_mid", "recon_end"]
 
     def profile_chain(self, tile, first, count):
-        ms = np.zeros(11, np.float64)
-        cnt = np.zeros(11, np.int64)
+        ms = np.zeros(len(self.PASS_KINDS), np.float64)
+        cnt = np.zeros(len(self.PASS_KINDS), np.int64)
         self._ck(lib.ptycho_profile_chain(self.h, tile, first, count, ms.ctypes.data, cnt.ctypes.data))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PASS_KINDS) if cnt[i]}
 
