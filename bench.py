@@ -252,6 +252,30 @@ def main():
     value = cfg.n_probes / (ms / 1e3)
     loss = p.iterate(want_loss=True)   # F(V) after K+W+1 iterations (untimed; sanity)
 
+    # ---- APPP exchange alone (N > 1): the four passes over all S slices, CUDA events on the
+    # context stream, max over ranks; bytes = cross-rank hop regions x S x 4 B (NVLink roofline)
+    appp = None
+    if world > 1:
+        from paper_2205_06327_b200.ptycho import appp_schedule
+        xbytes = sum((y1 - y0) * (x1 - x0) * S * 4 for (a, b, y0, y1, x0, x1, _) in appp_schedule(H, W, R, C, halo)
+                     if owner[a] != owner[b] and y1 > y0 and x1 > x0)
+        for _ in range(2):
+            p.appp_passes()
+        barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(5):
+            p.appp_passes()
+        a1.record(stream)
+        barrier()
+        t = torch.tensor([a0.elapsed_time(a1) / 5], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ams = float(t.item())
+        appp = {"transport": p.appp_transport(), "ms_per_call": ams, "cross_rank_bytes": xbytes,
+                "achieved_gbs_per_gpu": xbytes / world / (ams * 1e6), "nvlink_peak_gbs_per_gpu": 900.0,
+                "note": "not pipelined behind the backward here; in ptycho_iterate the slabs overlap it"}
+
     # ---- roofline of the dominant kernel (backward middle pass), CUDA events on its stream
     peak, peak_kind = hbm_peak()
     my_tiles = [k for k in range(ntiles) if owner[k] == rank]
@@ -339,7 +363,7 @@ def main():
                            "workspace_gb_per_gpu": ws / 1e9,
                            "adjoint": "stash-free (phi recomputed)" if args.stash_free else "stash"},
                 "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
-                "e2e": e2e, "cpu_baseline": cpu, "loss_after": loss,
+                "e2e": e2e, "cpu_baseline": cpu, "loss_after": loss, "appp": appp,
                 "paper_context": "GD small LT: 2310 probe-locations/s on 462 V100 (P:65-74)"}
         print(json.dumps(line), flush=True)
     p.close()

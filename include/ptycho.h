@@ -195,10 +195,27 @@ ptycho_status ptycho_forward_grad(ptycho_ctx ctx, int64_t first, int64_t count, 
 /* Alg. 1 steps 10-13 (Fig. forward_backward; APPP P:33-57): vertical
  * forward (ADD chains down tile columns), vertical backward (REPLACE chains up), horizontal
  * forward / backward over the full extended height (reading #21), on AccBuf.  Rank-local
- * tile pairs are device copies; cross-rank hops are NCCL send/recv, issued by every rank in
+ * tile pairs are device copies; cross-rank hops use the transport below, issued by every rank in
  * one global hop order with no barrier (a rank proceeds to its horizontal hops as soon as its
  * vertical ones are done: cross-direction pipelining).  Collective. */
 ptycho_status ptycho_appp_passes(ptycho_ctx ctx);
+
+/* Transport of cross-rank APPP hops.  PTYCHO_APPP_P2P: the receiving rank's copy
+ * kernel reads the sender's AccBuf region in place over NVLink (CUDA IPC mapping of the sender's
+ * workspace, exchanged once over the NCCL communicator) and adds / copies it into its own AccBuf;
+ * a READY / DONE flag pair per hop (system-scope release/acquire) replaces the send/recv
+ * handshake -- no pack, no staging buffer.  PTYCHO_APPP_NCCL: pack + ncclSend / ncclRecv +
+ * unpack.  PTYCHO_APPP_AUTO (default; env PTYCHO_APPP_TRANSPORT=nccl|p2p overrides): P2P when
+ * every rank can map every peer, else NCCL.  The choice is made collectively at the first APPP
+ * call and is the same on every rank; set it before that call (ESTATE after).  Requesting P2P
+ * where it is unavailable makes that first APPP call fail with ECUDA.  Results are bit-identical
+ * for both transports (same ADD order). */
+#define PTYCHO_APPP_AUTO 0
+#define PTYCHO_APPP_NCCL 1
+#define PTYCHO_APPP_P2P 2
+ptycho_status ptycho_set_appp_transport(ptycho_ctx ctx, int32_t mode);
+/* Active transport (PTYCHO_APPP_NCCL / _P2P), or PTYCHO_APPP_AUTO before the first APPP call. */
+ptycho_status ptycho_appp_transport(ptycho_ctx ctx, int32_t* mode);
 
 /* Alg. 1 steps 14-16: V_k -= alpha_acc * AccBuf_k ; AccBuf_k = 0. */
 ptycho_status ptycho_step(ptycho_ctx ctx);

@@ -3,6 +3,7 @@
 //
 // Paper anchors: Alg. 1, §Image Gradient Decomposition, §Forward and
 // Backward Accumulated Gradients Pass, APPP.
+#include <cuda.h>  // driver types for cuMemGetAddressRange (resolved through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -109,6 +110,16 @@ struct ptycho_ctx_s {
   bool persist = false;  // run probe chains in the persistent cooperative chain kernel
   bool batched = false;  // opt-in batched schedule (non-overlapping windows side by side)
   int batch = 1;         // batch slots per tile
+  // APPP transport between ranks (decided, collectively, at the first APPP call)
+  int transport_req = PTYCHO_APPP_AUTO;
+  int transport = PTYCHO_APPP_NCCL;
+  bool transport_set = false;
+  unsigned* flags = nullptr;  // [2][hops] READY / DONE epochs (P2P transport), in the workspace
+  unsigned epoch = 0;         // APPP calls so far (identical on every rank)
+  std::vector<char*> peer_ws;                   // [rank] peer workspace mapped into this process
+  std::vector<void*> peer_map;                  // opened IPC mappings (closed at destroy)
+  std::vector<long long> peer_flags;            // [rank] flags offset in that rank's workspace
+  std::vector<std::vector<long long>> peer_acc; // [rank][tile] AccBuf offset (-1: not owned)
 };
 
 static thread_local std::string g_create_err;
@@ -173,6 +184,10 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   if (const char* e = getenv("PTYCHO_SLAB")) ctx->slab = std::max(0, atoi(e));
   if (const char* e = getenv("PTYCHO_PERSIST")) ctx->persist = atoi(e) != 0;
   if (cfg->flags & PTYCHO_F_STASH_FREE) ctx->persist = false;  // the chain kernel keeps a full stash
+  if (const char* e = getenv("PTYCHO_APPP_TRANSPORT")) {
+    if (!strcmp(e, "nccl")) ctx->transport_req = PTYCHO_APPP_NCCL;
+    else if (!strcmp(e, "p2p")) ctx->transport_req = PTYCHO_APPP_P2P;
+  }
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -205,6 +220,7 @@ extern "C" ptycho_status ptycho_destroy(ptycho_ctx ctx) {
     for (cudaEvent_t e : t.slab_ev) cudaEventDestroy(e);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  for (void* m : ctx->peer_map) cudaIpcCloseMemHandle(m);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   delete ctx;
   return PTYCHO_OK;
@@ -457,6 +473,7 @@ static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
     ctx->msg_floats = std::max(mx, (size_t)(16u << 20));
     ctx->sendbuf = (float*)take(ctx->msg_floats * sizeof(float));
     ctx->recvbuf = (float*)take(ctx->msg_floats * sizeof(float));
+    ctx->flags = (unsigned*)take(2 * std::max<size_t>(ctx->hops.size(), 1) * sizeof(unsigned));
   }
   for (int k : ctx->local) {
     Tile& t = ctx->tiles[k];
@@ -525,6 +542,8 @@ extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_de
     CK(cudaMemsetAsync(t.amp, 0, std::max<size_t>(t.probes.size(), 1) * n * n * sizeof(float), ctx->stream));
   }
   PASS(zero_tiles(ctx, true, true));
+  if (ctx->flags) CK(cudaMemsetAsync(ctx->flags, 0, 2 * std::max<size_t>(ctx->hops.size(), 1) * sizeof(unsigned),
+                                     ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));  // host vectors above go out of scope
   ctx->ws_set = true;
   return PTYCHO_OK;
@@ -1112,15 +1131,153 @@ static ptycho_status hop_remote(ptycho_ctx ctx, const Hop& h, bool sender, int z
   return PTYCHO_OK;
 }
 
+// P2P transport (SURVEY §8(e) "fused"): the receiver's copy2d reads the sender's AccBuf region
+// in place through the CUDA IPC mapping of the sender's workspace (NVLink) and adds / copies it
+// into its own AccBuf -- no pack, no staging, no NCCL.  READY / DONE flags (kernels.cu) order the
+// two ranks exactly as a blocking send/recv pair would.
+static ptycho_status hop_p2p(ptycho_ctx ctx, const Hop& h, size_t hid, bool sender, int z0, int z1,
+                             unsigned ep) {
+  const size_t nh = ctx->hops.size();
+  const Tile& a = ctx->tiles[h.src];
+  const Tile& b = ctx->tiles[h.dst];
+  auto peer_flag = [&](int r, int which) {
+    return (unsigned*)(ctx->peer_ws[r] + ctx->peer_flags[r]) + which * nh + hid;
+  };
+  if (sender) {
+    CK(launch_p2p_signal(peer_flag(b.owner, 0), ep, ctx->flags + nh + hid, ctx->stream));
+    ++ctx->launches;
+    return PTYCHO_OK;
+  }
+  CK(launch_p2p_wait(ctx->flags + hid, ep, ctx->stream));
+  ++ctx->launches;
+  float* src_acc = (float*)(ctx->peer_ws[a.owner] + ctx->peer_acc[a.owner][a.k]);
+  for (int par = 0; par < 2; ++par) {
+    SliceView vs = region_view(a, src_acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    SliceView vd = region_view(b, b.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    if (vs.nslices == 0) continue;
+    CK(launch_copy2d(vd.base, vd.ld, vd.ss, vs.base, vs.ld, vs.ss, vs.rows, vs.cols, vs.nslices, h.add, ctx->stream));
+    ++ctx->launches;
+  }
+  CK(launch_p2p_post(peer_flag(a.owner, 1), ep, ctx->stream));
+  ++ctx->launches;
+  return PTYCHO_OK;
+}
+
+// Decide the APPP transport once, collectively: P2P needs every rank to map every other rank's
+// workspace (CUDA IPC on the allocation that holds it) with peer access; otherwise (or on request)
+// NCCL send/recv.  All ranks take the same decision (second all-gather of the verdicts).
+static ptycho_status appp_transport_setup(ptycho_ctx ctx) {
+  if (ctx->transport_set) return PTYCHO_OK;
+  ctx->transport_set = true;
+  ctx->transport = PTYCHO_APPP_NCCL;
+  if (ctx->nranks == 1 || ctx->transport_req == PTYCHO_APPP_NCCL) return PTYCHO_OK;
+  const int nr = ctx->nranks, nt = (int)ctx->tiles.size();
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    long long ws_off, flags_off;
+    int device, ok;
+  };
+  const size_t rec = align_up(sizeof(Rec) + nt * sizeof(long long), 8);
+  std::vector<char> mine(rec, 0), all(rec * nr, 0);
+  Rec* r = (Rec*)mine.data();
+  r->ok = 1;
+  r->device = ctx->device;
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  GetRange get_range = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUdeviceptr base = 0;
+  size_t sz = 0;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", (void**)&get_range, cudaEnableDefault, &q) != cudaSuccess ||
+      !get_range || get_range(&base, &sz, (CUdeviceptr)ctx->ws) != CUDA_SUCCESS ||
+      cudaIpcGetMemHandle(&r->h, (void*)base) != cudaSuccess) {
+    r->ok = 0;
+    cudaGetLastError();
+  }
+  r->ws_off = (long long)(ctx->ws - (char*)base);
+  r->flags_off = (long long)((char*)ctx->flags - ctx->ws);
+  long long* acc = (long long*)(mine.data() + sizeof(Rec));
+  for (const Tile& t : ctx->tiles) acc[t.k] = t.owner == ctx->rank ? (long long)((char*)t.acc - ctx->ws) : -1;
+  char* dsend = (char*)ctx->staging;
+  char* drecv = dsend + align_up(rec);
+  CK(cudaMemcpyAsync(dsend, mine.data(), rec, cudaMemcpyHostToDevice, ctx->stream));
+  NK(ncclAllGather(dsend, drecv, rec, ncclUint8, ctx->comm, ctx->stream));
+  CK(cudaMemcpyAsync(all.data(), drecv, rec * nr, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int ok = 1;
+  ctx->peer_ws.assign(nr, nullptr);
+  ctx->peer_flags.assign(nr, 0);
+  ctx->peer_acc.assign(nr, std::vector<long long>(nt, -1));
+  for (int j = 0; j < nr && ok; ++j) {
+    const Rec* o = (const Rec*)(all.data() + rec * j);
+    ok &= o->ok;
+    ctx->peer_flags[j] = o->flags_off;
+    const long long* oa = (const long long*)(all.data() + rec * j + sizeof(Rec));
+    for (int k = 0; k < nt; ++k) ctx->peer_acc[j][k] = oa[k];
+    if (j == ctx->rank) {
+      ctx->peer_ws[j] = ctx->ws;
+      continue;
+    }
+    int can = 0;
+    if (o->device == ctx->device || cudaDeviceCanAccessPeer(&can, ctx->device, o->device) != cudaSuccess || !can) {
+      ok = 0;
+      break;
+    }
+    void* m = nullptr;
+    if (cudaIpcOpenMemHandle(&m, o->h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      ok = 0;
+      break;
+    }
+    ctx->peer_map.push_back(m);
+    ctx->peer_ws[j] = (char*)m + o->ws_off;
+  }
+  cudaGetLastError();
+  // every rank must agree
+  int* dv = (int*)dsend;
+  CK(cudaMemcpyAsync(dv, &ok, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  NK(ncclAllGather(dv, dv + 64, 1, ncclInt32, ctx->comm, ctx->stream));
+  std::vector<int> votes(nr, 0);
+  CK(cudaMemcpyAsync(votes.data(), dv + 64, nr * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  bool all_ok = true;
+  for (int v : votes) all_ok &= v != 0;
+  if (all_ok) {
+    ctx->transport = PTYCHO_APPP_P2P;
+    return PTYCHO_OK;
+  }
+  for (void* m : ctx->peer_map) cudaIpcCloseMemHandle(m);
+  ctx->peer_map.clear();
+  if (ctx->transport_req == PTYCHO_APPP_P2P)
+    return fail(ctx, PTYCHO_ECUDA, "APPP P2P transport requested but some rank cannot map its peers");
+  return PTYCHO_OK;
+}
+
 // The four passes on the slices [z0, z1) of every AccBuf (every rank walks the same hop list).
 static ptycho_status appp_range(ptycho_ctx ctx, int z0, int z1) {
-  for (const Hop& h : ctx->hops) {
+  PASS(appp_transport_setup(ctx));
+  const bool p2p = ctx->transport == PTYCHO_APPP_P2P;
+  const unsigned ep = ++ctx->epoch;
+  for (size_t hid = 0; hid < ctx->hops.size(); ++hid) {
+    const Hop& h = ctx->hops[hid];
     if (h.y1 <= h.y0 || h.x1 <= h.x0) continue;  // disjoint extended rects: empty message
     const int so = ctx->tiles[h.src].owner, d = ctx->tiles[h.dst].owner;
     if (so == ctx->rank && d == ctx->rank) PASS(hop_local(ctx, h, z0, z1));
-    else if (so == ctx->rank) PASS(hop_remote(ctx, h, true, z0, z1));
-    else if (d == ctx->rank) PASS(hop_remote(ctx, h, false, z0, z1));
+    else if (so == ctx->rank) PASS(p2p ? hop_p2p(ctx, h, hid, true, z0, z1, ep) : hop_remote(ctx, h, true, z0, z1));
+    else if (d == ctx->rank) PASS(p2p ? hop_p2p(ctx, h, hid, false, z0, z1, ep) : hop_remote(ctx, h, false, z0, z1));
   }
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_set_appp_transport(ptycho_ctx ctx, int32_t mode) {
+  if (!ctx) return PTYCHO_EARG;
+  if (mode < PTYCHO_APPP_AUTO || mode > PTYCHO_APPP_P2P) return fail(ctx, PTYCHO_EARG, "transport %d", mode);
+  if (ctx->transport_set) return fail(ctx, PTYCHO_ESTATE, "the APPP transport is fixed at the first APPP call");
+  ctx->transport_req = mode;
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_appp_transport(ptycho_ctx ctx, int32_t* mode) {
+  if (!ctx || !mode) return PTYCHO_EARG;
+  *mode = ctx->transport_set ? ctx->transport : PTYCHO_APPP_AUTO;
   return PTYCHO_OK;
 }
 

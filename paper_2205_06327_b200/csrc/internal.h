@@ -102,5 +102,9 @@ cudaError_t launch_set_batch(int4* desc, const int2* centers, const int* list, i
 cudaError_t launch_set_desc(int4* desc, const int2* centers, int v, int nk, int n, cudaStream_t stream);
 cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t stream);
 cudaError_t launch_sum_double(const double* parts, int n, double* out, cudaStream_t stream);
+// APPP peer-to-peer transport: flag kernels (one thread each; see kernels.cu)
+cudaError_t launch_p2p_signal(unsigned* remote_ready, unsigned epoch, const unsigned* local_done, cudaStream_t s);
+cudaError_t launch_p2p_wait(const unsigned* local_ready, unsigned epoch, cudaStream_t s);
+cudaError_t launch_p2p_post(unsigned* remote_done, unsigned epoch, cudaStream_t s);
 
 }  // namespace ptycho

@@ -1036,16 +1036,30 @@ cudaError_t launch_pass(int n, PassKind kind, const PassArgs& a, cudaStream_t st
 // ------------------------------------------------------------------------------------------
 
 // dst[z][r][c] (op)= src[z][r][c], strided rows; grid (ceil(cols/128), rows, nslices)
-__global__ void copy2d_kernel(float* __restrict__ dst, long long dld, long long dss,
-                              const float* __restrict__ src, long long sld, long long sss, int rows, int cols,
-                              int op) {
+// Each thread moves COPY_U elements of one row (loads first, then the stores: COPY_U independent
+// loads in flight per thread -- what a peer (NVLink) source needs to approach link bandwidth).
+constexpr int COPY_U = 4;
+__global__ void __launch_bounds__(256) copy2d_kernel(float* __restrict__ dst, long long dld, long long dss,
+                                                     const float* __restrict__ src, long long sld, long long sss,
+                                                     int rows, int cols, int op) {
   const int r = blockIdx.y;
   const long long z = blockIdx.z;
   float* d = dst + z * dss + (long long)r * dld;
   const float* s = src + z * sss + (long long)r * sld;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
-    if (op == 0) d[c] = s[c];
-    else d[c] += s[c];
+  const int c0 = blockIdx.x * (256 * COPY_U) + threadIdx.x;
+  float v[COPY_U];
+#pragma unroll
+  for (int u = 0; u < COPY_U; ++u) {
+    const int c = c0 + 256 * u;
+    v[u] = c < cols ? s[c] : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < COPY_U; ++u) {
+    const int c = c0 + 256 * u;
+    if (c < cols) {
+      if (op == 0) d[c] = v[u];
+      else d[c] += v[u];
+    }
   }
 }
 
@@ -1056,7 +1070,7 @@ cudaError_t launch_copy2d(float* dst, long long dld, long long dss, const float*
     const int nz = nslices - z0 < 65535 ? nslices - z0 : 65535;
     for (int r0 = 0; r0 < rows; r0 += 65535) {
       const int nr = rows - r0 < 65535 ? rows - r0 : 65535;
-      dim3 grid((cols + 255) / 256 < 8 ? (cols + 255) / 256 : 8, nr, nz);
+      dim3 grid((cols + 256 * COPY_U - 1) / (256 * COPY_U), nr, nz);
       copy2d_kernel<<<grid, 256, 0, stream>>>(dst + z0 * dss + (long long)r0 * dld, dld, dss,
                                               src + z0 * sss + (long long)r0 * sld, sld, sss, nr, cols, op);
     }
@@ -1209,6 +1223,57 @@ __global__ void sum_double_kernel(const double* parts, int n, double* out) {
 
 cudaError_t launch_sum_double(const double* parts, int n, double* out, cudaStream_t stream) {
   sum_double_kernel<<<1, 32, 0, stream>>>(parts, n, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// APPP peer-to-peer transport (SURVEY §8(e) "fused"): the receiver's copy kernel reads the
+// sender's AccBuf region straight from peer memory over NVLink (CUDA IPC mapping) and adds or
+// copies it in place -- no pack, no staging buffer, no NCCL.  One flag pair per hop orders the
+// two ranks: READY (sender -> receiver: the region is final) and DONE (receiver -> sender: the
+// region has been read, the sender may overwrite it).  Flags carry the APPP call's epoch, so they
+// never need resetting.  System-scope release/acquire; spins trap after 20 s instead of hanging.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const unsigned* flag, unsigned epoch) {
+  const unsigned long long t0 = globaltimer();
+  while ((int)(ld_acquire_sys(flag) - epoch) < 0) {
+    __nanosleep(64);
+    if (globaltimer() - t0 > 20000000000ull) __trap();
+  }
+}
+
+// sender: publish "region final" to the receiver, then wait until the receiver has read it
+__global__ void p2p_signal_kernel(unsigned* remote_ready, unsigned epoch, const unsigned* local_done) {
+  __threadfence_system();  // AccBuf writes of the preceding kernels (stream order) before READY
+  st_release_sys(remote_ready, epoch);
+  spin_until(local_done, epoch);
+}
+// receiver: wait for READY (the copy kernel that follows on the stream then reads peer memory)
+__global__ void p2p_wait_kernel(const unsigned* local_ready, unsigned epoch) { spin_until(local_ready, epoch); }
+// receiver: after the copy kernel, tell the sender its region may be overwritten
+__global__ void p2p_post_kernel(unsigned* remote_done, unsigned epoch) {
+  __threadfence_system();
+  st_release_sys(remote_done, epoch);
+}
+
+cudaError_t launch_p2p_signal(unsigned* remote_ready, unsigned epoch, const unsigned* local_done, cudaStream_t s) {
+  p2p_signal_kernel<<<1, 1, 0, s>>>(remote_ready, epoch, local_done);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_wait(const unsigned* local_ready, unsigned epoch, cudaStream_t s) {
+  p2p_wait_kernel<<<1, 1, 0, s>>>(local_ready, epoch);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_post(unsigned* remote_done, unsigned epoch, cudaStream_t s) {
+  p2p_post_kernel<<<1, 1, 0, s>>>(remote_done, epoch);
   return cudaGetLastError();
 }
 

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("PTYCHO_LIB", os.path.join(_HERE, "lib", "libptycho.so
 
 PTYCHO_F_EXACT_WINDOW = 1
 PTYCHO_F_STASH_FREE = 2
+PTYCHO_APPP_AUTO, PTYCHO_APPP_NCCL, PTYCHO_APPP_P2P = 0, 1, 2
 PTYCHO_AMP_DC_CENTERED = 1
 PTYCHO_AMP_INTENSITY = 2
 STATUS = {0: "OK", 1: "EARG", 2: "ESHAPE", 3: "ESTATE", 4: "EHALO", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
@@ -60,6 +61,8 @@ _SIGS = {
     "ptycho_simulate_measurements": [_P],
     "ptycho_forward_grad": [_P, _c.c_int64, _c.c_int64, _c.POINTER(_c.c_double)],
     "ptycho_appp_passes": [_P],
+    "ptycho_set_appp_transport": [_P, _c.c_int32],
+    "ptycho_appp_transport": [_P, _c.POINTER(_c.c_int32)],
     "ptycho_step": [_P],
     "ptycho_iterate": [_P, _c.POINTER(_c.c_double)],
     "ptycho_stitch": [_P, _P, _c.c_int, _c.c_int32],
@@ -247,6 +250,15 @@ class Ptycho:
 
     def appp_passes(self):
         self._ck(lib.ptycho_appp_passes(self.h))
+
+    def set_appp_transport(self, mode):
+        """PTYCHO_APPP_AUTO / _NCCL / _P2P (before the first APPP call)."""
+        self._ck(lib.ptycho_set_appp_transport(self.h, mode))
+
+    def appp_transport(self):
+        v = ctypes.c_int32()
+        self._ck(lib.ptycho_appp_transport(self.h, ctypes.byref(v)))
+        return {0: "auto", 1: "nccl", 2: "p2p"}[v.value]
 
     def step(self):
         self._ck(lib.ptycho_step(self.h))

@@ -39,8 +39,9 @@ def run(grid, owner, nid, rank, world, device, iters=2, period=0):
     p.set_volume(0.5 * vt)
     losses = [p.iterate(want_loss=True) for _ in range(iters)]
     out = p.stitch(root=0, rank=rank)
+    transport = p.appp_transport()
     p.close()
-    return out, losses
+    return out, losses, transport
 
 
 def main():
@@ -55,12 +56,16 @@ def main():
         owner = [k * world // nt for k in range(nt)]
         obj = [Ptycho.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        multi, lm = run(grid, owner, obj[0], rank, world, local, period=period)
+        multi, lm, tr = run(grid, owner, obj[0], rank, world, local, period=period)
+        want = os.environ.get("PTYCHO_APPP_TRANSPORT")
+        if want in ("nccl", "p2p") and tr != want:
+            print(f"rank {rank}: APPP transport {tr}, requested {want}", flush=True)
+            ok = False
         if rank == 0:
-            single, ls = run(grid, None, None, 0, 1, local, period=period)
+            single, ls, _ = run(grid, None, None, 0, 1, local, period=period)
             same = np.array_equal(multi, single) and lm == ls
-            print(f"grid {grid} T={period}: multi-GPU == single-GPU virtual tiles: {same}; losses {lm} {ls}",
-                  flush=True)
+            print(f"grid {grid} T={period} transport {tr}: multi-GPU == single-GPU virtual tiles: {same}; "
+                  f"losses {lm} {ls}", flush=True)
             ok &= same
         dist.barrier()
     # APPP integer bit-exactness across ranks
@@ -82,12 +87,14 @@ def main():
             p.debug_write_tile(k, 1, init[k])
     p.appp_passes()
     p.synchronize()
+    if os.environ.get("PTYCHO_APPP_TRANSPORT") in ("nccl", "p2p"):
+        ok &= p.appp_transport() == os.environ["PTYCHO_APPP_TRANSPORT"]
     total = O.global_sum([b.astype(np.float64) for b in init], tiles, slices, *shape)
     mine = all(np.array_equal(p.debug_read_tile(k, 1).astype(np.float64),
                               total[:, tiles[k]["ext"][0]:tiles[k]["ext"][2], tiles[k]["ext"][1]:tiles[k]["ext"][3]])
                for k in range(nt) if owner[k] == rank)
     flags = [None] * world
-    dist.all_gather_object(flags, mine)
+    dist.all_gather_object(flags, mine and ok)
     if rank == 0:
         print(f"APPP integer check over {world} ranks: {flags}", flush=True)
         ok &= all(flags)

@@ -1,5 +1,5 @@
-"""Multi-GPU path (one process per GPU, APPP hops over NCCL): bit-identical to virtual tiles on
-one GPU.  Runs only where >= 2 GPUs are visible."""
+"""Multi-GPU path (one process per GPU; APPP hops over NCCL send/recv or the P2P pull transport):
+bit-identical to virtual tiles on one GPU.  Runs only where >= 2 GPUs are visible."""
 import os
 import subprocess
 import sys
@@ -15,13 +15,15 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_multi_gpu_bit_identical(world):
+def test_multi_gpu_bit_identical(world, transport):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world), os.path.join(ROOT, "tests", "mgpu_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, PTYCHO_APPP_TRANSPORT=transport)
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     print(out.stdout[-4000:], out.stderr[-4000:])
     assert out.returncode == 0
     assert "MGPU OK" in out.stdout
