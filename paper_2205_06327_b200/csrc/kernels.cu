@@ -452,7 +452,7 @@ struct Smem {
 // after griddepcontrol.wait).  PERSIST = true: one step of chain_kernel (tables and twiddles
 // already resident, probe passed in, input written by other CTAs before the grid barrier, read
 // through L2).
-template <int N, int KIND, bool PERSIST>
+template <int N, int KIND, bool PERSIST, bool TWG = false>
 __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4 pd,
                                           const float2 (&twr)[EngOf<N>::type::T * EngOf<N>::type::T == N
                                                                   ? EngOf<N>::type::E : 1],
@@ -471,13 +471,15 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   float2* pst = (float2*)(lbase + SM::ex_b);                // prefetched stash row (GRAD)
   float* pv = (float*)(lbase + SM::ex_b + SM::st_b);        // prefetched V row / amplitude row
   float* pacc = (float*)(lbase + SM::ex_b + SM::st_b + SM::v_b);  // prefetched AccBuf row (GRAD)
-  constexpr bool TW_REG = (ENG::T * ENG::T == N);
+  // TWG: twiddles read from the global table through L1 at every transform (no registers, no
+  // shared memory) -- the 4-CTA/SM forward build
+  constexpr bool TW_REG = (ENG::T * ENG::T == N) && !TWG;
   if constexpr (PERSIST) __syncthreads();  // the previous step's staging reads of smem are done
 
   // ---- before the grid dependency: tables, and prefetches of data written >= 2 kernels ago
   // tables: asynchronous copies (no register round trip); waited for with the other prefetches
   if constexpr (!PERSIST) {
-    if constexpr (!TW_REG)
+    if constexpr (!TW_REG && !TWG)
       for (int e = threadIdx.x; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
     for (int e = threadIdx.x; e < N / 4 + 1; e += L * Q) cp_async16((float4*)ht + e, (const float4*)a.htab + e);
   }
@@ -729,8 +731,9 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     if constexpr (TW_REG) {
       ENG::fft_r(x, ex, q, twr);
     } else {
-      if (f & 1) ENG::dif(x, ex, q, tw, bid);
-      else ENG::dit(x, ex, q, tw, bid);
+      const float2* twp = TWG ? a.wtab : tw;
+      if (f & 1) ENG::dif(x, ex, q, twp, bid);
+      else ENG::dit(x, ex, q, twp, bid);
     }
   }
   step(PL.post, PL.nf & 1);
@@ -811,11 +814,12 @@ __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KI
 pass_kernel(const PassArgs a) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T;
-  constexpr bool TW_REG = (ENG::T * ENG::T == N);
+  constexpr bool TWG = MINB >= 4 && !kind_grad(KIND) && ENG::T * ENG::T == N;
+  constexpr bool TW_REG = (ENG::T * ENG::T == N) && !TWG;
   extern __shared__ __align__(16) unsigned char smem[];
   const int q = threadIdx.x % Q;
   // four-step engines keep the thread's twiddles in registers (no shared-memory table)
-  float2 twr[TW_REG ? P : 1];
+  float2 twr[ENG::T * ENG::T == N ? P : 1];
   if constexpr (TW_REG) {
 #pragma unroll
     for (int k = 0; k < P; ++k) twr[k] = __ldg(a.wtab + k * Q + q);
@@ -825,7 +829,7 @@ pass_kernel(const PassArgs a) {
   constexpr int groups = N / LINES_PER_CTA;
   const int b = blockIdx.x / groups, grp = blockIdx.x - b * groups;
   if (b == 0) {
-    pass_body<N, KIND, false>(a, grp, make_int4(0, 0, 0, 0), twr, smem);
+    pass_body<N, KIND, false, TWG>(a, grp, make_int4(0, 0, 0, 0), twr, smem);
   } else {
     PassArgs ab = a;
     ab.stash += b * a.stash_slot;
@@ -833,7 +837,7 @@ pass_kernel(const PassArgs a) {
     ab.out += b * a.wf_slot;
     ab.desc += b;
     ab.loss_part += b * groups;
-    pass_body<N, KIND, false>(ab, grp, make_int4(0, 0, 0, 0), twr, smem);
+    pass_body<N, KIND, false, TWG>(ab, grp, make_int4(0, 0, 0, 0), twr, smem);
   }
 }
 
@@ -1019,7 +1023,10 @@ static cudaError_t launch_pass_nm(PassKind kind, const PassArgs& a, cudaStream_t
 
 template <int N>
 static cudaError_t launch_pass_n(PassKind kind, const PassArgs& a, cudaStream_t s, bool pdl) {
-  return a.high_occupancy ? launch_pass_nm<N, 3>(kind, a, s, pdl) : launch_pass_nm<N, 2>(kind, a, s, pdl);
+#ifndef PTYCHO_FWD_MINB
+#define PTYCHO_FWD_MINB 3
+#endif
+  return a.high_occupancy ? launch_pass_nm<N, PTYCHO_FWD_MINB>(kind, a, s, pdl) : launch_pass_nm<N, 2>(kind, a, s, pdl);
 }
 
 cudaError_t launch_pass(int n, PassKind kind, const PassArgs& a, cudaStream_t stream, bool pdl) {
