@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--stash-free", action="store_true",
                     help="stash-free adjoint (PTYCHO_F_STASH_FREE): phi_s recomputed, 2-slice stash")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-async", action="store_true",
+                    help="e2e: PTYCHO_AMP_ASYNC load overlapping the chains (measured slower on B200)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -184,7 +186,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2205_06327_b200.ptycho import Ptycho, PTYCHO_F_STASH_FREE
+    from paper_2205_06327_b200.ptycho import Ptycho, PTYCHO_F_STASH_FREE, PTYCHO_AMP_ASYNC
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -330,7 +332,7 @@ def main():
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.e2e_steps):
-            p.load_measurements(host_amp)
+            p.load_measurements(host_amp, flags=PTYCHO_AMP_ASYNC if args.e2e_async else 0)
             p.iterate()
             p.stitch(host_v, root=0, rank=rank)
         f1.record(stream)

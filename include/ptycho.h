@@ -62,6 +62,15 @@ typedef enum {
 /* ptycho_load_measurements layout_flags */
 #define PTYCHO_AMP_DC_CENTERED 1 /* input has DC at (N/2,N/2): ifftshift once at load           */
 #define PTYCHO_AMP_INTENSITY 2   /* input is |y|^2: take the square root at load                 */
+#define PTYCHO_AMP_ASYNC 4       /* host input, no layout change needed (no DC_CENTERED/INTENSITY, */
+                                 /* S even): return once the copies are enqueued.  They go straight */
+                                 /* into the stores on a copy stream in chunks of 8 probes, and each */
+                                 /* probe chain waits only for its own chunk, so the transfer        */
+                                 /* overlaps the gradient passes.  The host buffer (pinned for real  */
+                                 /* asynchrony) must stay valid and unchanged until                  */
+                                 /* ptycho_synchronize.  Otherwise the flag is ignored (synchronous). */
+                                 /* Measured on B200 (LT-small, 8 tiles): the overlapped copy slows  */
+                                 /* the chains by more than it saves (10.09 vs 9.84 s per e2e step). */
 
 typedef struct {
   int32_t n;         /* N: probe window = detector side; 64, 256 or 1024                          */

@@ -57,6 +57,16 @@ struct Tile {
   cudaGraphExec_t graph_b = nullptr;     // chain over `batch` slots, no cursor advance
   int64_t bfirst = -1, bcount = -1;      // cached batches for local probes [bfirst, bfirst+bcount)
   std::vector<std::vector<int>> batches;
+  // asynchronous measurement loads (PTYCHO_AMP_ASYNC): chunk [begin, ...) of the tile's store is
+  // complete when ev fires; chains wait only for the chunk holding their probe
+  struct AmpChunk {
+    int64_t begin;
+    cudaEvent_t ev;
+  };
+  std::vector<AmpChunk> amp_pend;
+  size_t amp_cur = 0;
+  std::vector<cudaEvent_t> amp_pool;
+  cudaEvent_t amp_free = nullptr;  // the tile stream's readers of the store are done
 };
 
 constexpr size_t ALIGN = 256;
@@ -120,6 +130,8 @@ struct ptycho_ctx_s {
   std::vector<void*> peer_map;                  // opened IPC mappings (closed at destroy)
   std::vector<long long> peer_flags;            // [rank] flags offset in that rank's workspace
   std::vector<std::vector<long long>> peer_acc; // [rank][tile] AccBuf offset (-1: not owned)
+  cudaStream_t copy_stream = nullptr;           // asynchronous measurement loads
+  cudaEvent_t ev_copy = nullptr;
 };
 
 static thread_local std::string g_create_err;
@@ -218,7 +230,11 @@ extern "C" ptycho_status ptycho_destroy(ptycho_ctx ctx) {
     if (t.stream) cudaStreamDestroy(t.stream);
     if (t.ev) cudaEventDestroy(t.ev);
     for (cudaEvent_t e : t.slab_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : t.amp_pool) cudaEventDestroy(e);
+    if (t.amp_free) cudaEventDestroy(t.amp_free);
   }
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   for (void* m : ctx->peer_map) cudaIpcCloseMemHandle(m);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -572,6 +588,80 @@ extern "C" ptycho_status ptycho_set_probe(ptycho_ctx ctx, const void* probe_c64,
   return PTYCHO_OK;
 }
 
+// Asynchronous host load straight into the measurement stores (no staging, no layout change): on
+// the copy stream, after every earlier reader of the stores; one event per chunk of probes.
+static ptycho_status load_async(ptycho_ctx ctx, const float* amp, int64_t first_local, int64_t count) {
+  const size_t n2 = (size_t)ctx->cfg.n * ctx->cfg.n;
+  if (!ctx->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(ctx->ev_copy, ctx->stream));  // e.g. set_workspace's clearing of the stores
+  CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_copy, 0));
+  int64_t chunk = 8;  // probes per event (32 MiB at N = 1024)
+  if (const char* e = getenv("PTYCHO_AMP_CHUNK")) chunk = std::max(1, atoi(e));
+  struct Range {
+    Tile* t;
+    int64_t g, lo, hi;
+  };
+  std::vector<Range> rs;
+  int64_t g = 0;
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const int64_t nk = (int64_t)t.probes.size();
+    const int64_t lo = std::max(first_local, g), hi = std::min(first_local + count, g + nk);
+    if (lo < hi) {
+      // chunks of an earlier load not yet consumed: later chains wait for all of them
+      while (t.amp_cur < t.amp_pend.size()) CK(cudaStreamWaitEvent(t.stream, t.amp_pend[t.amp_cur++].ev, 0));
+      t.amp_pend.clear();
+      t.amp_cur = 0;
+      if (!t.amp_free) CK(cudaEventCreateWithFlags(&t.amp_free, cudaEventDisableTiming));
+      CK(cudaEventRecord(t.amp_free, t.stream));  // chains still reading the store finish first
+      CK(cudaStreamWaitEvent(ctx->copy_stream, t.amp_free, 0));
+      rs.push_back({&t, g, lo, hi});
+    }
+    g += nk;
+  }
+  // round-robin over the tiles (the tiles' chains run concurrently and consume in probe order)
+  for (size_t ne = 0;; ++ne) {
+    bool any = false;
+    for (Range& r : rs) {
+      const int64_t p = r.lo + (int64_t)ne * chunk;
+      if (p >= r.hi) continue;
+      any = true;
+      Tile& t = *r.t;
+      const int64_t m = std::min(chunk, r.hi - p);
+      CK(cudaMemcpyAsync(t.amp + (size_t)(p - r.g) * n2, amp + (size_t)(p - first_local) * n2,
+                         (size_t)m * n2 * sizeof(float), cudaMemcpyHostToDevice, ctx->copy_stream));
+      if (ne == t.amp_pool.size()) {
+        t.amp_pool.push_back(nullptr);
+        CK(cudaEventCreateWithFlags(&t.amp_pool.back(), cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(t.amp_pool[ne], ctx->copy_stream));
+      t.amp_pend.push_back({p - r.g, t.amp_pool[ne]});
+    }
+    if (!any) break;
+  }
+  return PTYCHO_OK;
+}
+
+// Stream st waits for the pending asynchronous chunks of tile t that hold probes <= upto.
+static ptycho_status amp_wait(ptycho_ctx ctx, Tile& t, int64_t upto, cudaStream_t st) {
+  while (t.amp_cur < t.amp_pend.size() && t.amp_pend[t.amp_cur].begin <= upto)
+    CK(cudaStreamWaitEvent(st, t.amp_pend[t.amp_cur++].ev, 0));
+  if (t.amp_cur == t.amp_pend.size()) {
+    t.amp_pend.clear();
+    t.amp_cur = 0;
+  }
+  return PTYCHO_OK;
+}
+
+// Stream st waits for every pending asynchronous chunk of every local tile.
+static ptycho_status amp_settle(ptycho_ctx ctx, cudaStream_t st) {
+  for (int k : ctx->local) PASS(amp_wait(ctx, ctx->tiles[k], INT64_MAX, st));
+  return PTYCHO_OK;
+}
+
 extern "C" ptycho_status ptycho_load_measurements(ptycho_ctx ctx, const float* amp, int on_device,
                                                   int64_t first_local, int64_t count, int32_t layout_flags) {
   PASS(need_ws(ctx));
@@ -588,6 +678,9 @@ extern "C" ptycho_status ptycho_load_measurements(ptycho_ctx ctx, const float* a
   const int shift = (layout_flags & PTYCHO_AMP_DC_CENTERED) ? 1 : 0;
   const int inten = (layout_flags & PTYCHO_AMP_INTENSITY) ? 1 : 0;
   const int transpose = ctx->cfg.slices & 1;  // store in the turnaround pass's layout L_{S&1}
+  if ((layout_flags & PTYCHO_AMP_ASYNC) && !on_device && !shift && !inten && !transpose)
+    return load_async(ctx, amp, first_local, count);
+  PASS(amp_settle(ctx, ctx->stream));  // earlier asynchronous copies land before this load
   const int64_t chunk = (int64_t)(ctx->staging_floats / n2);
   int64_t g = 0;  // local index of the first probe of the current tile
   for (int k : ctx->local) {
@@ -620,6 +713,7 @@ extern "C" ptycho_status ptycho_read_measurements(ptycho_ctx ctx, float* amp_out
   if (count == 0) return PTYCHO_OK;
   if (!amp_out) return fail(ctx, PTYCHO_EARG, "amp_out is NULL");
   CK(cudaSetDevice(ctx->device));
+  if (ctx->copy_stream) CK(cudaStreamSynchronize(ctx->copy_stream));
   for (int k : ctx->local) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
   const int n = ctx->cfg.n;
   const size_t n2 = (size_t)n * n;
@@ -986,6 +1080,7 @@ static ptycho_status run_chain_kernel(ptycho_ctx ctx, int64_t first, const std::
   c.maxn = (int)maxn;
   c.S = ctx->cfg.slices;
   c.bar = (unsigned*)ctx->iscratch;
+  PASS(amp_settle(ctx, ctx->stream));
   CK(cudaMemsetAsync(ctx->iscratch, 0, sizeof(unsigned), ctx->stream));
   CK(launch_chain(ctx->cfg.n, c, ctx->stream));
   ctx->launches += 1;
@@ -1016,6 +1111,7 @@ static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, Ch
       Tile& t = ctx->tiles[k];
       const int64_t nk = (int64_t)t.probes.size();
       if (first + j >= nk) continue;
+      PASS(amp_wait(ctx, t, first + j, t.stream));
       if (mode == CHAIN_GRAD && t.graph) {
         CK(cudaGraphLaunch(t.graph, t.stream));
         ctx->launches += chain_len(ctx->cfg.slices, stash_free(ctx->cfg));
@@ -1028,6 +1124,7 @@ static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, Ch
 
 static ptycho_status run_batched(ptycho_ctx ctx, int64_t first, int64_t count) {
   PASS(fork_tiles(ctx));
+  for (int k : ctx->local) PASS(amp_wait(ctx, ctx->tiles[k], INT64_MAX, ctx->tiles[k].stream));
   size_t maxb = 0;
   for (int k : ctx->local) {
     Tile& t = ctx->tiles[k];
@@ -1342,6 +1439,7 @@ static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t co
     for (int k : ctx->local) {
       Tile& t = ctx->tiles[k];
       if (j >= m[k] || j < done[k]) continue;
+      PASS(amp_wait(ctx, t, first + j, t.stream));
       if (j < m[k] - 1 && t.graph) {
         CK(cudaGraphLaunch(t.graph, t.stream));
         ctx->launches += chain_len(S, stash_free(ctx->cfg));
@@ -1442,6 +1540,7 @@ extern "C" ptycho_status ptycho_synchronize(ptycho_ctx ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   for (int k : ctx->local)
     if (ctx->tiles[k].stream) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
+  if (ctx->copy_stream) CK(cudaStreamSynchronize(ctx->copy_stream));
   return PTYCHO_OK;
 }
 
@@ -1510,6 +1609,7 @@ static ptycho_status debug_chain(ptycho_ctx ctx, int tile, int64_t probe, ChainM
   if (probe < 0 || probe >= (int64_t)t->probes.size()) return fail(ctx, PTYCHO_EARG, "bad probe %lld", (long long)probe);
   CK(cudaSetDevice(ctx->device));
   PASS(zero_loss(ctx));
+  PASS(amp_settle(ctx, ctx->stream));
   PASS(set_cursor(ctx, *t, (int)probe, ctx->stream));
   PASS(enqueue_chain(ctx, *t, mode, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1552,6 +1652,7 @@ extern "C" ptycho_status ptycho_profile_chain(ptycho_ctx ctx, int32_t tile, int6
   CK(cudaStreamSynchronize(ctx->stream));
   PASS(set_cursor(ctx, *t, (int)first, t->stream));
   ChainProfile prof;
+  PASS(amp_settle(ctx, t->stream));
   for (int64_t j = 0; j < m; ++j) PASS(enqueue_chain(ctx, *t, CHAIN_GRAD, t->stream, &prof));
   CK(cudaStreamSynchronize(t->stream));
   for (size_t i = 0; i < prof.kind.size(); ++i) {

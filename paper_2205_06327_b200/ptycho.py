@@ -22,6 +22,7 @@ PTYCHO_F_STASH_FREE = 2
 PTYCHO_APPP_AUTO, PTYCHO_APPP_NCCL, PTYCHO_APPP_P2P = 0, 1, 2
 PTYCHO_AMP_DC_CENTERED = 1
 PTYCHO_AMP_INTENSITY = 2
+PTYCHO_AMP_ASYNC = 4
 STATUS = {0: "OK", 1: "EARG", 2: "ESHAPE", 3: "ESTATE", 4: "EHALO", 5: "ECUDA", 6: "ENCCL", 7: "ENOMEM"}
 
 

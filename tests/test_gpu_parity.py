@@ -366,3 +366,44 @@ def test_stitch_to_device_and_tile_rects():
     assert np.array_equal(out.cpu().numpy(), v)
     for k, t in enumerate(O.tile_geometry(150, 131, 2, 3, 20)):
         assert p.tile_rect(k) == (t["ext"], t["interior"])
+
+
+@pytest.mark.parametrize("batched", [False, True])
+def test_async_measurement_load_bit_identical(batched):
+    """PTYCHO_AMP_ASYNC (copies straight into the stores, overlapping the chains; each chain waits
+    for its own chunk) == the synchronous load, bitwise -- including a second load with different
+    data issued while the previous iteration's chains may still read the stores."""
+    import torch
+    from paper_2205_06327_b200.ptycho import PTYCHO_AMP_ASYNC
+    n, s, h, w = 64, 4, 150, 131  # S even: the store needs no transposition
+    rng = np.random.default_rng(8)
+    probe = synth.probe(n, 8.0)
+    vt = rng.random((s, h, w)).astype(np.float32)
+    centers = synth.scan_centers(h, w, 5, 6)
+    d = dict(n=n, slices=s, height=h, width=w, sigma=0.3, prop_c=3.135)
+    full = (0, 0, h, w)
+    amps = np.stack([O.farfield_magnitude(probe, O.window(vt.astype(np.float64), full, tuple(cc), n), d["sigma"],
+                                          d["prop_c"]) for cc in centers]).astype(np.float32)
+    amps2 = (amps * 1.01).astype(np.float32)
+    outs = []
+    for flags in (0, PTYCHO_AMP_ASYNC):
+        p = make(d, rows=2, cols=3, alpha=1.0, period=3)
+        p.set_scan(centers)
+        if batched:
+            p.set_schedule(True, 4)
+        p.allocate_workspace()
+        p.set_probe(probe.astype(np.complex64))
+        ids = p.local_probes()
+        h1 = torch.from_numpy(amps[ids]).pin_memory()
+        h2 = torch.from_numpy(amps2[ids]).pin_memory()
+        p.set_volume(0.5 * vt)
+        losses = []
+        for hb in (h1, h2, h1):
+            p.load_measurements(hb, flags=flags)
+            losses.append(p.iterate(want_loss=True))
+        back = np.zeros_like(amps[ids])
+        p.read_measurements(0, len(ids), back)
+        outs.append((p.stitch(), losses, back))
+        p.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[1][2], amps[ids])
