@@ -49,6 +49,7 @@ struct Tile {
   unsigned* done = nullptr;
   double* loss_part = nullptr;
   cudaStream_t stream = nullptr;
+  bool own_stream = false;
   cudaEvent_t ev = nullptr;
   cudaGraphExec_t graph = nullptr;
   std::vector<cudaEvent_t> slab_ev;  // APPP slab pipelining (segment_pipelined)
@@ -227,7 +228,7 @@ extern "C" ptycho_status ptycho_destroy(ptycho_ctx ctx) {
   for (auto& t : ctx->tiles) {
     if (t.graph) cudaGraphExecDestroy(t.graph);
     if (t.graph_b) cudaGraphExecDestroy(t.graph_b);
-    if (t.stream) cudaStreamDestroy(t.stream);
+    if (t.stream && t.own_stream) cudaStreamDestroy(t.stream);
     if (t.ev) cudaEventDestroy(t.ev);
     for (cudaEvent_t e : t.slab_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : t.amp_pool) cudaEventDestroy(e);
@@ -379,9 +380,21 @@ extern "C" ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t 
   }
   build_hops(ctx->tiles, rows, cols, ctx->hops);
   CK(cudaSetDevice(ctx->device));
-  for (int k : ctx->local) {
-    CK(cudaStreamCreateWithFlags(&ctx->tiles[k].stream, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ctx->tiles[k].ev, cudaEventDisableTiming));
+  // At most G = 4 tile chains in flight (PTYCHO_TILE_STREAMS overrides): local tile i uses the
+  // stream of local tile i % G.  Each chain's live wavefields are 16 MiB (N = 1024); 4 of them
+  // stay in the 126 MB L2 next to the streaming traffic, 8 do not -- LT-small on one B200 with
+  // 8 virtual tiles: G = 3..5 452 probe-loc/s, G = 6 439, G = 8 439 (profiles/round1.md).
+  int groups = std::min<int>((int)ctx->local.size(), 4);
+  if (const char* e = getenv("PTYCHO_TILE_STREAMS")) groups = std::max(1, std::min(groups, atoi(e)));
+  for (size_t i = 0; i < ctx->local.size(); ++i) {
+    Tile& t = ctx->tiles[ctx->local[i]];
+    if ((int)i < groups) {
+      CK(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
+      t.own_stream = true;
+    } else {
+      t.stream = ctx->tiles[ctx->local[i % groups]].stream;
+    }
+    CK(cudaEventCreateWithFlags(&t.ev, cudaEventDisableTiming));
   }
   if (nranks > 1) {
     ncclUniqueId id;
