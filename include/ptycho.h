@@ -270,6 +270,12 @@ ptycho_status ptycho_debug_write_tile(ptycho_ctx ctx, int32_t tile, int32_t whic
 ptycho_status ptycho_debug_probe_grad(ptycho_ctx ctx, int32_t tile, int64_t probe, float* grad_out,
                                       double* loss_out);
 
+/* SURVEY §8(b) forms of the two exports above, by GLOBAL probe id (the tile of this rank that
+ * holds it is looked up; EARG if none): output pointers may be host or device memory
+ * (cudaMemcpyDefault). */
+ptycho_status ptycho_probe_grad(ptycho_ctx ctx, int64_t probe, float* g_out, double* loss_out);
+ptycho_status ptycho_probe_exitwave(ptycho_ctx ctx, int64_t probe, void* psi_out);
+
 /* Literal exit wave psi_S (propagated after the last slice, reading #5), complex64 [N][N]
  * natural window order, of probe `probe` of tile `tile` at the current V_k. */
 ptycho_status ptycho_debug_exit_wave(ptycho_ctx ctx, int32_t tile, int64_t probe, void* psi_out);

@@ -1648,6 +1648,44 @@ extern "C" ptycho_status ptycho_debug_exit_wave(ptycho_ctx ctx, int32_t tile, in
   return PTYCHO_OK;
 }
 
+// Global probe id -> (local tile holding it, index in that tile's list); EARG if not local.
+static ptycho_status find_probe(ptycho_ctx ctx, int64_t probe, int* tile, int64_t* local) {
+  for (int k : ctx->local) {
+    const auto& pr = ctx->tiles[k].probes;
+    const auto it = std::lower_bound(pr.begin(), pr.end(), probe);
+    if (it != pr.end() && *it == probe) {
+      *tile = k;
+      *local = it - pr.begin();
+      return PTYCHO_OK;
+    }
+  }
+  return fail(ctx, PTYCHO_EARG, "probe %lld is not assigned to a tile of this rank", (long long)probe);
+}
+
+extern "C" ptycho_status ptycho_probe_grad(ptycho_ctx ctx, int64_t probe, float* g_out, double* loss_out) {
+  PASS(need_run(ctx));
+  int tile = 0;
+  int64_t j = 0;
+  PASS(find_probe(ctx, probe, &tile, &j));
+  Tile* t = nullptr;
+  PASS(debug_chain(ctx, tile, j, CHAIN_DEBUG_GRAD, &t));
+  const size_t cnt = (size_t)ctx->cfg.slices * ctx->cfg.n * ctx->cfg.n;
+  if (g_out) CK(cudaMemcpy(g_out, ctx->debug, cnt * sizeof(float), cudaMemcpyDefault));
+  if (loss_out) PASS(sum_loss(ctx, loss_out));
+  return PTYCHO_OK;
+}
+
+extern "C" ptycho_status ptycho_probe_exitwave(ptycho_ctx ctx, int64_t probe, void* psi_out) {
+  PASS(need_run(ctx));
+  int tile = 0;
+  int64_t j = 0;
+  PASS(find_probe(ctx, probe, &tile, &j));
+  Tile* t = nullptr;
+  PASS(debug_chain(ctx, tile, j, CHAIN_DEBUG_EXIT, &t));
+  if (psi_out) CK(cudaMemcpy(psi_out, ctx->debug, (size_t)ctx->cfg.n * ctx->cfg.n * sizeof(float2), cudaMemcpyDefault));
+  return PTYCHO_OK;
+}
+
 extern "C" ptycho_status ptycho_profile_chain(ptycho_ctx ctx, int32_t tile, int64_t first, int64_t count,
                                               double* ms_out, int64_t* launches_out) {
   PASS(need_run(ctx));

@@ -74,6 +74,8 @@ _SIGS = {
     "ptycho_debug_write_tile": [_P, _c.c_int32, _c.c_int32, _P],
     "ptycho_debug_probe_grad": [_P, _c.c_int32, _c.c_int64, _P, _c.POINTER(_c.c_double)],
     "ptycho_debug_exit_wave": [_P, _c.c_int32, _c.c_int64, _P],
+    "ptycho_probe_grad": [_P, _c.c_int64, _P, _c.POINTER(_c.c_double)],
+    "ptycho_probe_exitwave": [_P, _c.c_int64, _P],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(lib, _name)
@@ -316,4 +318,18 @@ class Ptycho:
         n = self.cfg.n
         psi = np.zeros((n, n), np.complex64)
         self._ck(lib.ptycho_debug_exit_wave(self.h, tile, probe, psi.ctypes.data))
+        return psi
+
+    def probe_grad(self, probe, out=None):
+        """d f_i / d V over the full window of GLOBAL probe `probe` (host numpy or device tensor out)."""
+        n, s = self.cfg.n, self.cfg.slices
+        g = np.zeros((s, n, n), np.float32) if out is None else out
+        loss = ctypes.c_double()
+        self._ck(lib.ptycho_probe_grad(self.h, probe, _ptr(g), ctypes.byref(loss)))
+        return g, loss.value
+
+    def probe_exitwave(self, probe, out=None):
+        n = self.cfg.n
+        psi = np.zeros((n, n), np.complex64) if out is None else out
+        self._ck(lib.ptycho_probe_exitwave(self.h, probe, _ptr(psi)))
         return psi

@@ -71,3 +71,40 @@ def test_fullsize_sampled_update(name, tile, local):
     assert e_grad <= tol and e_acc <= tol and e_v <= 1e-6
     assert abs(f - f_ref) <= ftol * f_ref
     p.close()
+
+
+def test_fullsize_stash_free_gradient():
+    """LT-small (N = 1024, S = 100) sampled probe through the stash-free adjoint (2-slice stash
+    ring + phi recomputation) in the bench launch configuration; tolerance from the float32 floor
+    of the same recurrence (oracle.probe_grad_recompute)."""
+    from paper_2205_06327_b200.ptycho import Ptycho, PTYCHO_F_STASH_FREE
+    c = synth.CONFIGS["lt_small"]
+    n, s, h, w = c.n, c.slices, c.height, c.width
+    rows, cols = c.grid
+    tile, local = 5, 200
+    probe = synth.probe(n, c.defocus_nm)
+    vt = synth.volume(0, s, h, w)
+    v0 = (0.5 * vt).astype(np.float32)
+    centers = synth.scan_centers(h, w, c.scan_ny, c.scan_nx)
+    tiles = O.tile_geometry(h, w, rows, cols, n // 2)
+    asg = O.assign_probes(centers, tiles)
+    gid = asg[tile][local]
+    center = tuple(int(v) for v in centers[gid])
+    amp = O.farfield_magnitude(probe, O.window(vt.astype(np.float64), (0, 0, h, w), center, n), c.sigma, c.prop_c)
+    vwin = O.window(v0.astype(np.float64), (0, 0, h, w), center, n)
+    g_ref, f_ref = O.probe_grad(probe, vwin, amp, c.sigma, c.prop_c)
+    g32, _ = O.probe_grad_recompute(probe, vwin, amp, c.sigma, c.prop_c, dtype=np.float32)
+    floor = rel(g32, g_ref)
+    p = Ptycho(n, s, h, w, c.sigma, c.prop_c, alpha=0.5, flags=PTYCHO_F_STASH_FREE)
+    p.set_tiles(rows, cols, n // 2)
+    p.set_scan(centers)
+    p.allocate_workspace()
+    p.set_probe(probe.astype(np.complex64))
+    p.load_measurements(amp[None].astype(np.float32), first_local=sum(len(a) for a in asg[:tile]) + local)
+    p.set_volume(v0)
+    g, f = p.probe_grad(gid)
+    err = rel(g, g_ref)
+    print(f"lt_small stash-free tile {tile} probe {local}: grad {err:.2e} (recompute fp32 floor {floor:.2e}); "
+          f"loss rel {abs(f - f_ref) / f_ref:.2e}")
+    assert err <= max(1e-5, 2 * floor)
+    p.close()

@@ -407,3 +407,38 @@ def test_async_measurement_load_bit_identical(batched):
         p.close()
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
     assert np.array_equal(outs[1][2], amps[ids])
+
+
+def test_global_probe_exports_match_tile_exports():
+    """ptycho_probe_grad / ptycho_probe_exitwave (SURVEY §8(b) names, global probe id, host or
+    device output) == the per-tile debug exports, bitwise; a probe of another rank is EARG."""
+    import torch
+    from paper_2205_06327_b200.ptycho import PtychoError
+    d, probe, vt, centers, amps = _recon_problem()
+    p = make(d, rows=2, cols=3)
+    p.set_scan(centers)
+    p.allocate_workspace()
+    p.set_probe(probe.astype(np.complex64))
+    p.load_measurements(amps[p.local_probes()])
+    p.set_volume(0.5 * vt)
+    ids = list(p.local_probes())
+    for gid in (ids[0], ids[len(ids) // 2], ids[-1]):
+        tile = next(k for k in range(6) if gid in set(_tile_probes(p, k)))
+        j = _tile_probes(p, tile).index(gid)
+        g0, f0 = p.debug_probe_grad(tile, j)
+        g1, f1 = p.probe_grad(gid)
+        gd = torch.zeros((d["slices"], d["n"], d["n"]), dtype=torch.float32, device="cuda:0")
+        _, f2 = p.probe_grad(gid, out=gd)
+        assert np.array_equal(g0, g1) and np.array_equal(g0, gd.cpu().numpy()) and f0 == f1 == f2
+        assert np.array_equal(p.debug_exit_wave(tile, j), p.probe_exitwave(gid))
+    with pytest.raises(PtychoError) as e:
+        p.probe_grad(10 ** 6)
+    assert e.value.status == 1
+    p.close()
+
+
+def _tile_probes(p, k):
+    """Global ids of tile k's probes (ascending) = local_probes() restricted to the tile."""
+    lp = list(p.local_probes())
+    start = sum(p.tile_probe_count(t) for t in range(k))
+    return lp[start:start + p.tile_probe_count(k)]
