@@ -865,8 +865,11 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   a.sigma_pi = (float)((double)ctx->cfg.sigma / M_PI);
   a.alpha = ctx->cfg.alpha;
   a.thr = (float)(ctx->cfg.tau * ctx->probe_norm / ctx->cfg.n);
-  // >= 4 tile chains share the GPU: prefer the forward-pass build with room for more CTAs
-  a.high_occupancy = ctx->local.size() >= 4 ? 1 : 0;
+  // >= 2 tile chains share the GPU: the forward-pass build with room for more CTAs (same-box A/B,
+  // LT-small: 1 chain 374 vs 329 probe-loc/s for the 2-CTA build; 2 chains 446 vs 430 and 8 tiles
+  // 452 vs 425 for the 3-CTA build)
+  a.high_occupancy = ctx->local.size() >= 2 ? 1 : 0;
+  if (const char* e = getenv("PTYCHO_HIGH_OCC")) a.high_occupancy = atoi(e) != 0;  // A/B override
   a.batch = 1;  // the batched graph overrides (set_schedule)
   a.stash_slot = (long long)stash_slices(ctx->cfg) * ctx->cfg.n * ctx->cfg.n;
   a.stash_store = 1;

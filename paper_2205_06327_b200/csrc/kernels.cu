@@ -847,9 +847,9 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 }
 
 // MINB: CTAs per SM the register allocation must allow.  2: the single-chain-latency build
-// (a probe chain alone on the GPU: 2.65 ms/probe at N = 1024, S = 100); 3: forward passes at
-// <= 168 registers leave room for CTAs of other tiles' chains (8 concurrent tiles: +7%
-// probes/s, but a lone chain runs 12% slower).  The host picks per context (api.cu).  Backward
+// (a probe chain alone on the GPU: 2.67 ms/probe at N = 1024, S = 100); 3: forward passes at
+// <= 168 registers leave room for CTAs of other tiles' chains (2 chains +4 %, 8 tiles +6 %
+// probes/s, but a lone chain runs 12 % slower).  The host picks per context (api.cu).  Backward
 // passes always use 2 (they spill at 168).  Both builds execute the same arithmetic.
 template <int N, int KIND, int MINB>
 __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KIND) ? 2 : MINB)
