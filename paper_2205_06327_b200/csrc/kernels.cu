@@ -134,22 +134,35 @@ __device__ __forceinline__ void sincos_t(float x, float* sn, float* cs) {
 template <int P>
 struct EngFour {
   static constexpr int N = P * P, T = P, E = P;
-  static constexpr int EX = P * (P + 1);  // exchange buffer per line (float2)
+  // exchange buffer per line (float2): rows padded to P + 2 (16-B aligned rows) -- the column
+  // writes (STS.64) and the row reads (LDS.128, 8 threads per phase at a 4-bank stride) are both
+  // bank-conflict free
+  static constexpr int LD = P + 2;
+  static constexpr int EX = P * LD;
   static constexpr int TW = N;            // twiddle table (float2)
   __device__ __forceinline__ static int idx(int, int t, int k) { return t + T * k; }
   __device__ __forceinline__ static void sync_line(int) { __syncwarp(); }
+  // transpose of the P x P block held by the line's P threads (thread q: column q -> row q)
+  __device__ __forceinline__ static void exchange(float2 (&x)[E], float2* __restrict__ ex, int q) {
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < P; ++k) ex[k * LD + q] = x[k];
+    __syncwarp();
+    const float4* row = (const float4*)(ex + q * LD);
+#pragma unroll
+    for (int n = 0; n < P / 2; ++n) {
+      const float4 v = row[n];
+      x[2 * n] = make_float2(v.x, v.y);
+      x[2 * n + 1] = make_float2(v.z, v.w);
+    }
+    __syncwarp();
+  }
   __device__ __forceinline__ static void fft(float2 (&x)[E], float2* __restrict__ ex, int q,
                                             const float2* __restrict__ tw) {
     DftReg<P>::run(x);
 #pragma unroll
     for (int k = 1; k < P; ++k) x[k] = cmul(x[k], tw[k * P + q]);
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < P; ++k) ex[k * (P + 1) + q] = x[k];
-    __syncwarp();
-#pragma unroll
-    for (int n = 0; n < P; ++n) x[n] = ex[q * (P + 1) + n];
-    __syncwarp();
+    exchange(x, ex, q);
     DftReg<P>::run(x);
   }
   // same transform with the thread's P twiddles W_N^{qk} held in registers (loaded once per pass)
@@ -161,13 +174,7 @@ struct EngFour {
     DftReg<P>::run(x);
 #pragma unroll
     for (int k = 1; k < P; ++k) x[k] = cmul(x[k], twr[k]);
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < P; ++k) ex[k * (P + 1) + q] = x[k];
-    __syncwarp();
-#pragma unroll
-    for (int n = 0; n < P; ++n) x[n] = ex[q * (P + 1) + n];
-    __syncwarp();
+    exchange(x, ex, q);
     DftReg<P>::run(x);
   }
   __device__ __forceinline__ static void dit(float2 (&x)[E], float2* ex, int t, const float2* tw, int) {
