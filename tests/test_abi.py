@@ -40,3 +40,14 @@ def test_header_documents_every_call():
     for name in header_functions():
         i = src.index(name + "(")
         assert "/*" in src[max(0, i - 1200):i], f"{name} lacks a comment"
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """No CPU or PyTorch fallback: with the shared library missing, importing the binding raises."""
+    import subprocess
+    import sys
+    code = "import paper_2205_06327_b200.ptycho"
+    env = dict(os.environ, PTYCHO_LIB=str(tmp_path / "missing.so"))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT)
+    assert out.returncode != 0
+    assert "ImportError" in out.stderr or "OSError" in out.stderr
