@@ -442,3 +442,24 @@ def _tile_probes(p, k):
     lp = list(p.local_probes())
     start = sum(p.tile_probe_count(t) for t in range(k))
     return lp[start:start + p.tile_probe_count(k)]
+
+
+def test_appp_transport_api_states():
+    """set_appp_transport: EARG for an unknown mode, ESTATE once the first APPP call fixed the
+    transport; a single rank reports NCCL (no cross-rank hops) after that call."""
+    from paper_2205_06327_b200.ptycho import PtychoError, PTYCHO_APPP_P2P
+    d, probe, vt, centers, amps = _recon_problem()
+    p = make(d, rows=2, cols=3)
+    p.set_scan(centers)
+    p.allocate_workspace()
+    assert p.appp_transport() == "auto"
+    with pytest.raises(PtychoError) as e:
+        p.set_appp_transport(7)
+    assert e.value.status == 1
+    p.set_appp_transport(PTYCHO_APPP_P2P)  # allowed before the first APPP call; moot on one rank
+    p.appp_passes()
+    assert p.appp_transport() == "nccl"
+    with pytest.raises(PtychoError) as e:
+        p.set_appp_transport(PTYCHO_APPP_P2P)
+    assert e.value.status == 3
+    p.close()
