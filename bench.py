@@ -37,6 +37,22 @@ def env_int(k, d):
     return int(os.environ.get(k, d))
 
 
+def bind_to_gpu_numa(dev):
+    """Pin this rank's host threads to the CPUs local to its GPU (NVML), so the pinned host
+    buffers of the e2e leg are first-touched on the GPU's NUMA node.  Returns the CPU count or
+    None if NVML / the PCI id is unavailable (then nothing changes)."""
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        pynvml.nvmlInit()
+        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByPciBusId(bus))
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
@@ -192,6 +208,7 @@ def main():
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local_rank)
+    numa_cpus = bind_to_gpu_numa(local_rank) if world > 1 else None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
@@ -363,7 +380,8 @@ def main():
                            "alpha": alpha, "pass_period": "once per iteration",
                            "l2": "inputs > L2 (V_k+AccBuf 8.9 GB, |y| 17.4 GB)",
                            "workspace_gb_per_gpu": ws / 1e9,
-                           "adjoint": "stash-free (phi recomputed)" if args.stash_free else "stash"},
+                           "adjoint": "stash-free (phi recomputed)" if args.stash_free else "stash",
+                           "host_affinity": f"GPU-local NUMA node ({numa_cpus} CPUs)" if numa_cpus else "default"},
                 "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
                 "e2e": e2e, "cpu_baseline": cpu, "loss_after": loss, "appp": appp,
                 "paper_context": "GD small LT: 2310 probe-locations/s on 462 V100 (P:65-74)"}
