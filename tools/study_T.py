@@ -3,7 +3,9 @@ Fig. convergence: "once or twice per iteration converges slightly faster than ev
 
 F(V) (Eq. 1, summed over the sweep) per iteration for T in {every probe, twice per iteration,
 once per iteration}, in exact-window mode (halo N/2) and the paper's circle-halo mode (small halo,
-zero-extended windows, reading #13), on a 2x2 tile grid.  Writes profiles/round1_T_study.json."""
+zero-extended windows, reading #13), on a 2x2 tile grid.  Writes profiles/round1_T_study.json;
+CONFIG=appp runs the BASELINE "APPP check" shape instead (N = 256, S = 20, 1024^2 object, 64 x 64
+probes, circle halo 60 px = the paper's 600 pm) and writes profiles/round1_T_study_appp.json."""
 import json
 import os
 import sys
@@ -15,17 +17,24 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 from paper_2205_06327_b200.ptycho import Ptycho  # noqa: E402
 
-n, s, h, w = 64, 4, 256, 256
-ny = nx = 12
+CONFIG = os.environ.get("CONFIG", "")
+if CONFIG:
+    _c = synth.CONFIGS[CONFIG]
+    n, s, h, w, ny, nx, sigma, prop_c = _c.n, _c.slices, _c.height, _c.width, _c.scan_ny, _c.scan_nx, _c.sigma, _c.prop_c
+    defocus, circle_halo = _c.defocus_nm, 60
+else:
+    n, s, h, w = 64, 4, 256, 256
+    ny = nx = 12
+    sigma, prop_c, defocus, circle_halo = 0.1, 3.135, 8.0, 12
 iters = int(os.environ.get("ITERS", 40))
 alpha = float(os.environ.get("ALPHA", 0.5))
-probe = synth.probe(n, 8.0).astype(np.complex64)
+probe = synth.probe(n, defocus).astype(np.complex64)
 vt = synth.volume(1, s, h, w)
 centers = synth.scan_centers(h, w, ny, nx)
 
 
 def run(period, halo, grid=(2, 2)):
-    p = Ptycho(n, s, h, w, 0.1, 3.135, alpha=alpha, pass_period=period)
+    p = Ptycho(n, s, h, w, sigma, prop_c, alpha=alpha, pass_period=period)
     p.set_tiles(grid[0], grid[1], halo)
     p.set_scan(centers)
     p.allocate_workspace()
@@ -62,7 +71,7 @@ print("alpha =", alpha, flush=True)
 out = {"config": dict(n=n, slices=s, object=[h, w], probes=ny * nx, grid="2x2", alpha=alpha, iterations=iters,
                       v0="0", measurements="simulated |G(p, V_true)| (noise-free)"), "runs": []}
 nmax = None
-for halo, mode in [(n // 2, "exact-window"), (12, "circle-halo")]:
+for halo, mode in [(n // 2, "exact-window"), (circle_halo, "circle-halo")]:
     base = run(0, halo)
     nmax = base[0]
     for name, period in [("every probe (T=1)", 1), ("twice per iteration", -(-nmax // 2)), ("once per iteration", 0)]:
@@ -74,4 +83,5 @@ single = run(0, n // 2, grid=(1, 1))
 out["runs"].append(dict(mode="single tile", halo=0, T="once per iteration", period=0, F=single[1], rel_err_V=single[2]))
 print(f"{'single tile':13s} {'once per iteration':22s} F[-1]={single[1][-1]:.4e} |V-Vtrue|/|Vtrue|={single[2]:.4f}")
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-json.dump(out, open(os.path.join(ROOT, "profiles", "round1_T_study.json"), "w"), indent=1)
+name = f"round1_T_study_{CONFIG}.json" if CONFIG else "round1_T_study.json"
+json.dump(out, open(os.path.join(ROOT, "profiles", name), "w"), indent=1)
