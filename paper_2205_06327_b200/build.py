@@ -30,6 +30,8 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "ptycho.h")]
+    if not os.path.exists(DEMO) or os.path.getmtime(DEMO_SRC) > os.path.getmtime(DEMO):
+        return True
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -62,7 +64,25 @@ def build(force: bool = False, verbose: bool = True, defines=(), out=None) -> st
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.check_call(link)
+    if out is None:
+        build_demo(verbose)
     return lib_out
+
+
+DEMO_SRC = os.path.join(ROOT, "examples", "ptycho_demo.c")
+DEMO = os.path.join(LIBDIR, "ptycho_demo")
+
+
+def build_demo(verbose: bool = True) -> str:
+    """examples/ptycho_demo.c: plain C against include/ptycho.h + libptycho.so (no Python)."""
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    cmd = ["gcc", "-O2", "-std=c11", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"),
+           DEMO_SRC, "-o", DEMO, "-L", LIBDIR, "-lptycho", "-Wl,-rpath," + LIBDIR,
+           "-L", os.path.join(cuda, "lib64"), "-lcudart", "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-lm"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+    return DEMO
 
 
 if __name__ == "__main__":
