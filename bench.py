@@ -319,11 +319,23 @@ def main():
     achieved = bytes_bwd / t_bwd_step / 1e9 if t_bwd_step else None
     achieved_iso = bytes_bwd / t_bwd / 1e9 if t_bwd > 0 else None
     traffic = None
+    warp_inst = None
     try:
         summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         traffic = summ.get("bwd_mid", {}).get("dram_bytes_per_launch")
+        warp_inst = summ.get("bwd_mid", {}).get("warp_instructions")
     except Exception:
         pass
+    # The pass is issue/latency bound: the same in-step launch time against the
+    # instruction-issue roofline -- ncu's executed warp-instructions per launch over
+    # 148 SMs x 4 schedulers x 1 warp-instruction per clock at the SM clock sampled in the run.
+    issue = None
+    if warp_inst and t_bwd_step:
+        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        peak_issue = 148 * 4 * clk_mhz * 1e6
+        issue = {"achieved_warp_inst_per_s": warp_inst / t_bwd_step, "peak": peak_issue,
+                 "frac": warp_inst / t_bwd_step / peak_issue,
+                 "warp_instructions_per_launch": warp_inst, "source": "profiles/ncu_summary.json"}
     flops_pass = 4 * 5 * n * np.log2(n) * n  # nominal 5 n log2 n per 1-D transform, 4 transforms per line
     roofline = {"bound": "hbm", "kernel": "pass_kernel<1024, bwd_mid> (P^H, grad/AccBuf/SGD, P^H)",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
@@ -336,7 +348,8 @@ def main():
                 "fwd_mid": {"ms_per_launch_isolated": t_fwd * 1e3,
                             "achieved_gbs_isolated": bytes_fwd / t_fwd / 1e9 if t_fwd else None,
                             "fp32_tflops_nominal_isolated": flops_pass / t_fwd / 1e12 if t_fwd else None},
-                "chain_ms_per_probe_isolated": chain_ms / 4 if chain_ms else None}
+                "chain_ms_per_probe_isolated": chain_ms / 4 if chain_ms else None,
+                "issue": issue}
 
     # ---- e2e: host measurements (pinned) -> device, one iteration, stitched V -> host, each step
     e2e = None
