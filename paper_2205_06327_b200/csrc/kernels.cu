@@ -330,6 +330,13 @@ void fill_twiddles(int n, float2* tw) {
 //   adjoint      P^H = F^-1 conj(H)/N F  ->  F ; y <- (H/N) conj(y)      ; F ; result = conj(z)
 // so after the second F of a propagation the register value is the conjugate of the true field
 // ("conj pending"); the next step folds that conjugation in.
+// Unroll factor of the rolled pointwise steps (TRANSMIT / GRAD / RECON), see S_GRAD: 4 measured
+// +0.5 % over 2 (8 tiles and lone chain), 8 -1 % / -2 % (profiles/round1.md).
+#ifndef PTYCHO_STEP_UNROLL
+#define PTYCHO_STEP_UNROLL 4
+#endif
+constexpr int kStepUnroll = PTYCHO_STEP_UNROLL;
+
 enum Step : int {
   S_NONE = 0,
   S_HC_FWD,      // y <- conj(H) conj(y)            (inside P)
@@ -628,7 +635,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       float2* xs = ex + q;  // rolled through the idle exchange buffer (instruction-cache footprint)
 #pragma unroll
       for (int k = 0; k < P; ++k) xs[Q * k] = x[k];
-#pragma unroll 2
+#pragma unroll kStepUnroll
       for (int k = 0; k < P; ++k) {
         const float v = pv[q + Q * k];
         float sn, cs;
@@ -685,7 +692,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       float2* xs = ex;
 #pragma unroll
       for (int k = 0; k < P; ++k) xs[ENG::idx(dist, q, k)] = x[k];
-#pragma unroll 2
+#pragma unroll kStepUnroll
       for (int k = 0; k < P; ++k) {
         const int j = ENG::idx(dist, q, k);
         float2 phi = xs[j];
@@ -718,7 +725,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       float2* xs = ex;
 #pragma unroll
       for (int k = 0; k < P; ++k) xs[ENG::idx(dist, q, k)] = x[k];
-#pragma unroll 2
+#pragma unroll kStepUnroll
       for (int k = 0; k < P; ++k) {
         const int j = ENG::idx(dist, q, k);
         const int p = LL.pos0 + j;
