@@ -336,6 +336,14 @@ void fill_twiddles(int n, float2* tw) {
 #define PTYCHO_STEP_UNROLL 4
 #endif
 constexpr int kStepUnroll = PTYCHO_STEP_UNROLL;
+#ifndef PTYCHO_PREF_UNROLL
+#define PTYCHO_PREF_UNROLL 8
+#endif
+#ifndef PTYCHO_STORE_UNROLL
+#define PTYCHO_STORE_UNROLL 4
+#endif
+constexpr int kPrefUnroll = PTYCHO_PREF_UNROLL;    // V / AccBuf row prefetch loop
+constexpr int kStoreUnroll = PTYCHO_STORE_UNROLL;  // transposed-store loop
 
 enum Step : int {
   S_NONE = 0,
@@ -559,7 +567,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     const long long so = (long long)a.s * a.slice_stride + LL.row;
     const float* vrow = a.V + so;
     const float* arow = a.acc + so;
-#pragma unroll 4
+#pragma unroll kPrefUnroll
     for (int k = 0; k < P; ++k) {
       const int j = q + Q * k, p = LL.pos0 + j;
       if (LL.ok && (unsigned)p < (unsigned)LL.plim) {
@@ -827,7 +835,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     }
     __syncthreads();
     float2* dst = a.out + (size_t)grp * L;
-#pragma unroll 4
+#pragma unroll kStoreUnroll
     for (int e = threadIdx.x; e < N * 2; e += L * Q) {
       const int j = e >> 1, c = e & 1, sw = (j >> 2) & 3;
       float4 v = *(const float4*)(stg + j * 4 + 2 * c);
