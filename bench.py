@@ -191,8 +191,10 @@ def main():
     ap.add_argument("--stash-free", action="store_true",
                     help="stash-free adjoint (PTYCHO_F_STASH_FREE): phi_s recomputed, 2-slice stash")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--e2e-async", action="store_true",
-                    help="e2e: PTYCHO_AMP_ASYNC load overlapping the chains (measured slower on B200)")
+    ap.add_argument("--e2e-async", choices=["auto", "on", "off"], default="auto",
+                    help="e2e: PTYCHO_AMP_ASYNC load overlapping the chains; auto = on at >= 4 GPUs, "
+                         "where the ranks share the host's upload bandwidth (N=4: e2e +16 %%), off "
+                         "below (N=1: -2.5 %%, N=2: -8 %%); profiles/round1.md")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -354,6 +356,7 @@ def main():
     # ---- e2e: host measurements (pinned) -> device, one iteration, stitched V -> host, each step
     e2e = None
     if not args.no_e2e:
+        e2e_async = args.e2e_async == "on" or (args.e2e_async == "auto" and world >= 4)
         host_amp = torch.empty((nloc, n, n), dtype=torch.float32, pin_memory=True)
         p.read_measurements(0, nloc, host_amp)
         host_v = torch.empty((S, H, W), dtype=torch.float32, pin_memory=True) if rank == 0 else None
@@ -362,7 +365,7 @@ def main():
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.e2e_steps):
-            p.load_measurements(host_amp, flags=PTYCHO_AMP_ASYNC if args.e2e_async else 0)
+            p.load_measurements(host_amp, flags=PTYCHO_AMP_ASYNC if e2e_async else 0)
             p.iterate()
             p.stitch(host_v, root=0, rank=rank)
         f1.record(stream)
@@ -375,7 +378,7 @@ def main():
             ems = float(t.item())
         e2e = {"value": cfg.n_probes / (ems / 1e3), "unit": "probe-locations/s",
                "h2d_bytes_per_step": cfg.n_probes * n2 * 4, "d2h_bytes_per_step": S * H * W * 4,
-               "ms_per_step": ems, "steps": args.e2e_steps}
+               "ms_per_step": ems, "steps": args.e2e_steps, "async_upload": e2e_async}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
