@@ -427,3 +427,139 @@ def test_batched_schedule_is_exactly_sequential():
     assert np.array_equal(a, b)
     order = O.batch_order(list(range(36)), centers, (0, 0, 60, 60), 16, 3)
     assert sorted(order) == list(range(36)) and order != list(range(36))
+
+
+# ----------------------------------------------------------------------------- round-2 pins
+# VERDICT r1 "What's weak" 2: each test below names the plausible oracle slip it catches.
+
+def test_forward_single_slice_closed_form_transmit_then_propagate():
+    # S = 1 (reading #1): Psi = F F^-1 (H F(t p)) = H F(t p) and |H| = 1, so |Psi| = |DFT(e^{i sigma V} p)|
+    # exactly, for ANY propagator.  A propagate-then-transmit forward gives |DFT(t F^-1 H F p)|,
+    # which differs for a non-constant V.  Pinned against the naive DFT (not the oracle's fft2).
+    n, sigma, c = 32, 0.9, 3.135
+    rng = np.random.default_rng(21)
+    p = synth.probe(n, 8.0)
+    v = rng.random((1, n, n))
+    _, big_psi, _ = O.forward(p, v, sigma, c)
+    closed = np.abs(O.dft2_naive(np.exp(1j * sigma * v[0]) * p))
+    assert np.abs(np.abs(big_psi) - closed).max() < 1e-13
+    # negative control: the wrong order is far from the closed form
+    m = np.fft.fftfreq(n) * n
+    h = np.exp(-1j * np.pi * c * (m[:, None] ** 2 + m[None, :] ** 2) / n ** 2)
+    wrong = np.abs(O.dft2_naive(np.exp(1j * sigma * v[0]) * O.dft2_naive(h * O.dft2_naive(p), inverse=True)))
+    assert rel(wrong, closed) > 1e-3
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_fft_matches_naive_dft_at_parity_sizes(n):
+    # the parity tests use fft2 / ifft2 at N = 256 and 1024: pin them there against the O(N^3)
+    # separable naive DFT (dft2_naive is itself pinned to the O(N^4) brute force at N <= 8)
+    rng = np.random.default_rng(n)
+    x = crandn(rng, n, n)
+    assert rel(O.fft2(x), O.dft2_naive(x)) < 1e-12
+    assert rel(O.ifft2(x), O.dft2_naive(x, inverse=True)) < 1e-12
+
+
+def test_window_mask_brute_force_clipped_inside_object():
+    # R_k strictly inside the object (an interior tile's extended rect): the mask must follow R_k,
+    # not the object bounds (circle-halo clipping, reading #12)
+    ext = (10, 5, 40, 45)
+    n = 16
+    for center in [(12, 7), (39, 44), (25, 20), (0, 0), (47, 52), (10, 30)]:
+        m = O.window_mask(ext, center, n)
+        for j in range(n):
+            for l in range(n):
+                y, x = center[0] - n // 2 + j, center[1] - n // 2 + l
+                assert m[j, l] == (ext[0] <= y < ext[2] and ext[1] <= x < ext[3])
+
+
+def _grad_at(p, vk, ext, center, n, amp, cfg):
+    return O.probe_grad(p, O.window(vk, ext, center, n), amp, cfg["sigma"], cfg["prop_c"])[0]
+
+
+def _scatter_full(shape, ext, center, n, g):
+    out = np.zeros(shape)
+    O._scatter(out, ext, center, n, g, O.window_mask(ext, center, n), 1.0)
+    return out
+
+
+def test_reconstruct_two_probes_once_per_iteration_hand_composed():
+    # Alg. 1 steps 6-16 with one tile, two probes, passes once per iteration, alpha != alpha_acc:
+    #   g0 = g(V0); V <- V0 - a g0; g1 = g(V0 - a g0); V <- V - a g1; V <- V - a_acc (g0 + g1)
+    # Catches: alpha / alpha_acc swapped (g1 would be taken at V0 - a_acc g0), the step-8 update
+    # skipped (g1 at V0), AccBuf not accumulated across probes.
+    p, vt, _, cfg, _ = _tiny_problem(ny=1, nx=2)
+    centers = np.array([[20, 14], [21, 24]], np.int32)  # overlapping 16 x 16 windows
+    ext = O.tile_geometry(40, 40, 1, 1, 0)[0]["ext"]
+    amps = [O.farfield_magnitude(p, O.window(vt, ext, tuple(c), 16), 0.3, 1.0) for c in centers]
+    v0 = 0.5 * vt
+    ext = O.tile_geometry(40, 40, 1, 1, 0)[0]["ext"]
+    a, aa = 0.7, 0.2
+    c0, c1 = tuple(centers[0]), tuple(centers[1])
+    g0 = _scatter_full(v0.shape, ext, c0, 16, _grad_at(p, v0, ext, c0, 16, amps[0], cfg))
+    g1 = _scatter_full(v0.shape, ext, c1, 16, _grad_at(p, v0 - a * g0, ext, c1, 16, amps[1], cfg))
+    expect = v0 - a * g0 - a * g1 - aa * (g0 + g1)
+    out, _, _, accs = O.reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 1, alpha=a, alpha_acc=aa)
+    assert rel(out - v0, expect - v0) < 1e-10  # compared on the update, which is small next to V
+    assert np.abs(accs[0]).max() == 0.0  # step 16: AccBuf reset
+    swapped, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 1, alpha=aa, alpha_acc=a)
+    assert rel(swapped - v0, expect - v0) > 1e-4
+
+
+def test_reconstruct_two_iterations_every_probe_hand_composed():
+    # T = 1 (passes after every local probe), one probe, two iterations:
+    #   V1 = V0 - (a + a_acc) g(V0);  V2 = V1 - (a + a_acc) g(V1)
+    # An AccBuf that is not reset (step 16) would subtract a_acc g(V0) again in iteration 2.
+    p, vt, centers, cfg, amps = _tiny_problem(ny=1, nx=1)
+    v0 = 0.5 * vt
+    ext = O.tile_geometry(40, 40, 1, 1, 0)[0]["ext"]
+    a, aa = 0.05, 0.03
+    c0 = tuple(centers[0])
+    v1 = v0 - (a + aa) * _scatter_full(v0.shape, ext, c0, 16, _grad_at(p, v0, ext, c0, 16, amps[0], cfg))
+    v2 = v1 - (a + aa) * _scatter_full(v0.shape, ext, c0, 16, _grad_at(p, v1, ext, c0, 16, amps[0], cfg))
+    out, losses, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 2, alpha=a, alpha_acc=aa, period=1)
+    assert rel(out - v0, v2 - v0) < 1e-10
+    assert len(losses) == 2
+    g0 = _scatter_full(v0.shape, ext, c0, 16, _grad_at(p, v0, ext, c0, 16, amps[0], cfg))
+    no_reset = v2 - aa * g0  # what a missing step 16 would add in iteration 2
+    assert rel(no_reset - v0, v2 - v0) > 1e-2
+
+
+def test_reconstruct_multi_tile_segments_hand_composed():
+    # 2x1 tiles, exact-window halo, T = 3 (two pass segments per iteration: 3 and 1 local probes
+    # per tile for a 4x2 scan): within a segment each tile runs sequential SGD on its own V_k;
+    # then every tile adds the GLOBAL sum of the segment's AccBuf contributions (Eq. 2, P:205 --
+    # composed here with global_sum, not with the APPP chain) times a_acc.
+    n, s, h, w = 16, 2, 40, 28
+    rng = np.random.default_rng(31)
+    p = synth.probe(n, 3.0, aperture_frac=0.3)
+    vt = rng.random((s, h, w))
+    centers = synth.scan_centers(h, w, 4, 2)
+    cfg = dict(n=n, sigma=0.3, prop_c=1.0)
+    full = (0, 0, h, w)
+    amps = [O.farfield_magnitude(p, O.window(vt, full, tuple(c), n), 0.3, 1.0) for c in centers]
+    tiles = O.tile_geometry(h, w, 2, 1, n // 2)
+    asg = O.assign_probes(centers, tiles)
+    assert [len(x) for x in asg] == [4, 4]
+    a, aa, T = 0.2, 0.1, 3
+    v0 = 0.5 * vt
+    vks = O.decompose(v0, tiles)
+    for j in range(2):
+        contribs = []
+        for k, t in enumerate(tiles):
+            acc = np.zeros_like(vks[k])
+            for i in asg[k][j * T:(j + 1) * T]:
+                c = tuple(int(x) for x in centers[i])
+                g = _grad_at(p, vks[k], t["ext"], c, n, amps[i], cfg)
+                d = np.zeros_like(acc)
+                O._scatter(d, t["ext"], c, n, g, O.window_mask(t["ext"], c, n), 1.0)
+                acc += d
+                vks[k] = vks[k] - a * d
+            contribs.append(acc)
+        tot = O.global_sum(contribs, tiles, s, h, w)
+        for k, t in enumerate(tiles):
+            y0, x0, y1, x1 = t["ext"]
+            vks[k] = vks[k] - aa * tot[:, y0:y1, x0:x1]
+    expect = O.stitch(vks, tiles, s, h, w)
+    out, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 2, 1, n // 2, 1, alpha=a, alpha_acc=aa, period=T)
+    assert rel(out - v0, expect - v0) < 1e-10
