@@ -109,20 +109,78 @@ def workload_name(cfg):
             f"{cfg.width}x{cfg.height}x{cfg.slices} object")
 
 
-def cpu_oracle_sample(cfg, probe, vt, centers, n_probes=1):
-    """The float64 oracle, as it stands, on a bounded sample: the full forward + adjoint gradient
-    of `n_probes` probes of the workload (N=1024, S=100).  Returns (probes/s, seconds, sample)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _oracle_probe_worker(args):
+    """One probe's forward + adjoint gradient (oracle.probe_grad, float64) on a window of `slices`
+    slices: the unit of the CPU baseline.  Inputs are synthetic of the workload's shape (timing is
+    data-independent); numpy's FFT is single-threaded, so one worker = one core."""
+    n, slices, sigma, c, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import ptycho_oracle as O
-    full = (0, 0, cfg.height, cfg.width)
-    i0 = len(centers) // 2
+    rng = np.random.default_rng(seed)
+    probe = synth.probe(n, 25.0)
+    vwin = 0.5 * rng.random((slices, n, n))
+    amp = np.abs(np.fft.fft2(probe, norm="ortho"))
     t0 = time.perf_counter()
-    for i in range(i0, i0 + n_probes):
-        c = tuple(int(v) for v in centers[i])
-        vwin = O.window(vt, full, c, cfg.n).astype(np.float64)
-        amp = np.abs(np.fft.fft2(probe, norm="ortho"))  # any non-negative amplitude: timing is data-independent
-        O.probe_grad(probe, vwin * 0.5, amp, cfg.sigma, cfg.prop_c)
+    O.probe_grad(probe, vwin, amp, sigma, c)
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_sample(cfg, workers, slices_per_probe):
+    """The float64 oracle, as it stands, on a bounded sample of the workload: `workers` processes
+    (one per core) each compute one probe's forward + adjoint over `slices_per_probe` of the S
+    slices (the per-probe cost is linear in S, so the sample is slices_per_probe / S probe-locations
+    per worker).  Returns (probe-locations/s, wall seconds, sample text)."""
+    import multiprocessing as mp
+    frac = slices_per_probe / cfg.slices
+    jobs = [(cfg.n, slices_per_probe, cfg.sigma, cfg.prop_c, i) for i in range(workers)]
+    t0 = time.perf_counter()
+    if workers == 1:
+        _oracle_probe_worker(jobs[0])
+    else:
+        with mp.get_context("spawn").Pool(workers) as pool:
+            pool.map(_oracle_probe_worker, jobs, chunksize=1)
     dt = time.perf_counter() - t0
-    return n_probes / dt, dt, f"{n_probes} probe(s) of {cfg.name} (N={cfg.n}, S={cfg.slices}) forward+adjoint, float64"
+    return workers * frac / dt, dt, (f"{workers} x one {cfg.name} probe (N={cfg.n}) forward+adjoint over "
+                                     f"{slices_per_probe} of S={cfg.slices} slices (= {frac:g} probe-locations "
+                                     f"each), float64, one process per core")
+
+
+def cpu_workers():
+    """All host cores, capped by memory (one N=1024 probe over 25 slices needs ~0.7 GB)."""
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+        n = min(n, max(1, int(psutil.virtual_memory().available / 1.5e9)))
+    except Exception:
+        pass
+    return n
+
+
+def cpu_tiny_iteration():
+    """One full Alg. 1 iteration of the tiny config (BASELINE configs[0]) through oracle.reconstruct."""
+    from oracle import ptycho_oracle as O
+    c = synth.CONFIGS["tiny"]
+    probe = synth.probe(c.n, c.defocus_nm)
+    vt = synth.volume(0, c.slices, c.height, c.width).astype(np.float64)
+    centers = synth.scan_centers(c.height, c.width, c.scan_ny, c.scan_nx)
+    full = (0, 0, c.height, c.width)
+    amps = [O.farfield_magnitude(probe, O.window(vt, full, tuple(cc), c.n), c.sigma, c.prop_c) for cc in centers]
+    d = dict(n=c.n, sigma=c.sigma, prop_c=c.prop_c)
+    t0 = time.perf_counter()
+    O.reconstruct(0.5 * vt, probe, amps, centers, d, 1, 1, c.halo, 1, alpha=1.0)
+    dt = time.perf_counter() - t0
+    return {"config": "tiny (64^2 x 16 probes, 128^2 x 4 object, 1 tile)", "sec_per_iteration": dt,
+            "probe_locations_per_s": c.n_probes / dt, "cores": 1}
 
 
 def run_reference(args):
@@ -131,24 +189,24 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = synth.CONFIGS[args.config]
-    probe = synth.probe(cfg.n, cfg.defocus_nm)
-    vt = synth.volume(0, cfg.slices, cfg.height, cfg.width)
-    centers = synth.scan_centers(cfg.height, cfg.width, cfg.scan_ny, cfg.scan_nx)
+    workers = cpu_workers()
+    per = 25 if cfg.slices >= 25 else cfg.slices
     for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, probe, vt, centers, 1)
-    times = []
+        cpu_oracle_sample(cfg, workers, per)
+    vals, times = [], []
+    sample = ""
     for _ in range(args.steps):
-        _, dt, sample = cpu_oracle_sample(cfg, probe, vt, centers, 1)
+        v, dt, sample = cpu_oracle_sample(cfg, workers, per)
+        vals.append(v)
         times.append(dt)
-    sec = sum(times) / len(times)
-    value = 1.0 / sec
+    value = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "probe-locations/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": value / PAPER_BEST_LT_SMALL,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "sample": "1 probe per step (bounded sample of the iteration)"},
-            "cpu_baseline": {"value": value, "unit": "probe-locations/s", "cores": 1, "kind": "oracle",
-                             "sample": sample},
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": value / PAPER_BEST_LT_SMALL, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "sample": "per step: " + sample},
+            "cpu_baseline": {"value": value, "unit": "probe-locations/s", "cores": workers, "kind": "oracle",
+                             "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": "probe-locations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -309,8 +367,12 @@ def main():
     chain_ms = sum(v[0] for v in prof.values())
     t_bwd = bwd[0] / max(bwd[1], 1) * 1e-3
     t_fwd = fwd[0] / max(fwd[1], 1) * 1e-3
-    bytes_bwd = 24 * n2   # stash read 8N^2 + V rmw 8N^2 + AccBuf rmw 8N^2 (algorithmic, per launch)
-    bytes_fwd = 12 * n2   # V read 4N^2 + stash write 8N^2
+    # compulsory (algorithmic) HBM bytes of one backward middle pass = V read-modify-write
+    # 8N^2 + AccBuf read-modify-write 8N^2 = 16N^2; the stash read (8N^2) is a design byte (the
+    # stash-free adjoint removes it), reported beside it as "design"
+    bytes_bwd = 16 * n2
+    bytes_bwd_design = 24 * n2
+    bytes_fwd = 4 * n2    # V read (compulsory); + stash write 8N^2 = 12N^2 design
     # In the timed region the tile chains run as CUDA graphs with programmatic dependent launch
     # (and up to 8 tiles concurrently), so a launch's in-step duration is the step time the
     # kernel accounts for (its share of the chain, measured with CUDA events on the tile stream
@@ -339,19 +401,49 @@ def main():
                  "frac": warp_inst / t_bwd_step / peak_issue,
                  "warp_instructions_per_launch": warp_inst, "source": "profiles/ncu_summary.json"}
     flops_pass = 4 * 5 * n * np.log2(n) * n  # nominal 5 n log2 n per 1-D transform, 4 transforms per line
+    # whole-path fractions (SURVEY §8(d) "Roofline fractions reported"), G GPUs:
+    #   strict = probes/s x B_alg / (G x HBM), B_alg = 4N^2 (1 + 5S)  (|y|, V read fwd, V and AccBuf rmw bwd)
+    #   design = probes/s x B_des / (G x HBM), B_des = 12N^2 + 36N^2 S (+ stash write/read, probe)
+    #   fp32   = probes/s x 10 N^2 log2 N (4S - 2) / (G x FP32 peak), FP32 peak = SMs x 128 lanes x 2 flop
+    #            x sampled SM clock (no tensor cores on this path)
+    b_alg = 4 * n2 * (1 + 5 * S)
+    b_des = 12 * n2 + 36 * n2 * S
+    fft_flops = 10 * n2 * np.log2(n) * (4 * S - 2)
+    clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+    fp32_peak = sms * 128 * 2 * clk_mhz * 1e6
+    whole = {"strict": value * b_alg / (world * peak * 1e9), "design": value * b_des / (world * peak * 1e9),
+             "fp32": value * fft_flops / (world * fp32_peak), "b_alg_bytes_per_probe": b_alg,
+             "b_des_bytes_per_probe": b_des, "fft_flops_per_probe": fft_flops, "fp32_peak_tflops": fp32_peak / 1e12,
+             "hbm_peak_gbs": peak}
     roofline = {"bound": "hbm", "kernel": "pass_kernel<1024, bwd_mid> (P^H, grad/AccBuf/SGD, P^H)",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_bytes_per_launch": bytes_bwd,
+                "design": {"bytes_per_launch": bytes_bwd_design,
+                           "achieved": bytes_bwd_design / t_bwd_step / 1e9 if t_bwd_step else None,
+                           "frac": bytes_bwd_design / t_bwd_step / 1e9 / peak if t_bwd_step else None},
+                "whole_path": whole,
                 "ms_per_launch_in_step": t_bwd_step * 1e3 if t_bwd_step else None,
                 "share_of_chain": share, "launches_per_step": bwd_launches_step,
                 "isolated": {"ms_per_launch": t_bwd * 1e3, "achieved_gbs": achieved_iso,
                              "frac": achieved_iso / peak if achieved_iso else None},
                 "fwd_mid": {"ms_per_launch_isolated": t_fwd * 1e3,
+                            "algorithmic_bytes_per_launch": bytes_fwd,
                             "achieved_gbs_isolated": bytes_fwd / t_fwd / 1e9 if t_fwd else None,
                             "fp32_tflops_nominal_isolated": flops_pass / t_fwd / 1e12 if t_fwd else None},
                 "chain_ms_per_probe_isolated": chain_ms / 4 if chain_ms else None,
                 "issue": issue}
+
+    # ---- per-rank runtime breakdown (the paper's Fig. runtime_breakdown,
+    # P:427-430): one more real iteration with serial phases, CUDA events on each rank's stream
+    bd = p.profile_iteration()
+    bd["rank"] = rank
+    breakdown = [bd]
+    if world > 1:
+        allbd = [None] * world
+        dist.all_gather_object(allbd, bd)
+        breakdown = allbd
 
     # ---- e2e: host measurements (pinned) -> device, one iteration, stitched V -> host, each step
     e2e = None
@@ -382,9 +474,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, dt, sample = cpu_oracle_sample(cfg, probe, vt, centers, 1)
-        cpu = {"value": v, "unit": "probe-locations/s", "cores": 1, "kind": "oracle", "sample": sample,
-               "seconds": dt}
+        workers = cpu_workers()
+        per = 25 if S >= 25 else S
+        v, dt, sample = cpu_oracle_sample(cfg, workers, per)
+        v1, dt1, sample1 = cpu_oracle_sample(cfg, 1, per)
+        cpu = {"value": v, "unit": "probe-locations/s", "cores": workers, "kind": "oracle", "sample": sample,
+               "seconds": dt, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+               "one_thread": {"value": v1, "seconds": dt1, "sample": sample1},
+               "tiny_full_iteration": cpu_tiny_iteration()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "probe-locations/s", "n_gpus": world,
@@ -399,6 +496,8 @@ def main():
                            "adjoint": "stash-free (phi recomputed)" if args.stash_free else "stash",
                            "host_affinity": f"GPU-local NUMA node ({numa_cpus} CPUs)" if numa_cpus else "default"},
                 "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
+                "breakdown": {"note": "one extra iteration, APPP slab pipelining off (phases serial); ms per rank",
+                              "ranks": breakdown},
                 "e2e": e2e, "cpu_baseline": cpu, "loss_after": loss, "appp": appp,
                 "paper_context": "GD small LT: 2310 probe-locations/s on 462 V100 (P:65-74)"}
         print(json.dumps(line), flush=True)

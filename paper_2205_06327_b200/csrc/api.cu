@@ -133,9 +133,14 @@ struct ptycho_ctx_s {
   std::vector<std::vector<long long>> peer_acc; // [rank][tile] AccBuf offset (-1: not owned)
   cudaStream_t copy_stream = nullptr;           // asynchronous measurement loads
   cudaEvent_t ev_copy = nullptr;
+  unsigned* p2p_err = nullptr;                  // pinned, mapped: a P2P flag wait timed out
+  unsigned* p2p_err_dev = nullptr;
+  unsigned long long p2p_timeout_ns = 600ull * 1000000000ull;
+  std::vector<cudaEvent_t>* wait_ev = nullptr;  // ptycho_profile_iteration: events around P2P waits
 };
 
 static thread_local std::string g_create_err;
+static ptycho_status check_p2p(ptycho_ctx ctx);
 
 static ptycho_status fail(ptycho_ctx ctx, ptycho_status st, const char* fmt, ...) {
   char buf[1024];
@@ -197,6 +202,7 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   if (const char* e = getenv("PTYCHO_SLAB")) ctx->slab = std::max(0, atoi(e));
   if (const char* e = getenv("PTYCHO_PERSIST")) ctx->persist = atoi(e) != 0;
   if (cfg->flags & PTYCHO_F_STASH_FREE) ctx->persist = false;  // the chain kernel keeps a full stash
+  if (const char* e = getenv("PTYCHO_P2P_TIMEOUT_S")) ctx->p2p_timeout_ns = (unsigned long long)(atof(e) * 1e9);
   if (const char* e = getenv("PTYCHO_APPP_TRANSPORT")) {
     if (!strcmp(e, "nccl")) ctx->transport_req = PTYCHO_APPP_NCCL;
     else if (!strcmp(e, "p2p")) ctx->transport_req = PTYCHO_APPP_P2P;
@@ -225,6 +231,14 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
 extern "C" ptycho_status ptycho_destroy(ptycho_ctx ctx) {
   if (!ctx) return PTYCHO_OK;
   cudaSetDevice(ctx->device);
+  // Drain every stream the library queued work on before any handle goes away (the caller frees
+  // the workspace right after).  Peers that mapped this workspace are done with it as well: a
+  // sender's stream cannot pass its READY/DONE hop before the receiver has posted DONE.
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (int k : ctx->local)
+    if (ctx->tiles[k].stream) cudaStreamSynchronize(ctx->tiles[k].stream);
+  if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+  if (ctx->p2p_err) cudaFreeHost(ctx->p2p_err);
   for (auto& t : ctx->tiles) {
     if (t.graph) cudaGraphExecDestroy(t.graph);
     if (t.graph_b) cudaGraphExecDestroy(t.graph_b);
@@ -1060,6 +1074,7 @@ static ptycho_status sum_loss(ptycho_ctx ctx, double* out_host) {
   std::vector<double> h(std::max(j, 1), 0.0);
   if (j) CK(cudaMemcpyAsync(h.data(), ctx->dscratch, j * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  PASS(check_p2p(ctx));
   double tot = 0.0;
   for (int i = 0; i < j; ++i) tot += h[i];
   *out_host = tot;
@@ -1257,11 +1272,21 @@ static ptycho_status hop_p2p(ptycho_ctx ctx, const Hop& h, size_t hid, bool send
     return (unsigned*)(ctx->peer_ws[r] + ctx->peer_flags[r]) + which * nh + hid;
   };
   if (sender) {
-    CK(launch_p2p_signal(peer_flag(b.owner, 0), ep, ctx->flags + nh + hid, ctx->stream));
+    CK(launch_p2p_signal(peer_flag(b.owner, 0), ep, ctx->flags + nh + hid, ctx->p2p_timeout_ns, ctx->p2p_err_dev,
+                         ctx->stream));
     ++ctx->launches;
     return PTYCHO_OK;
   }
-  CK(launch_p2p_wait(ctx->flags + hid, ep, ctx->stream));
+  cudaEvent_t w0 = nullptr, w1 = nullptr;
+  if (ctx->wait_ev) {
+    CK(cudaEventCreate(&w0));
+    CK(cudaEventCreate(&w1));
+    ctx->wait_ev->push_back(w0);
+    ctx->wait_ev->push_back(w1);
+    CK(cudaEventRecord(w0, ctx->stream));
+  }
+  CK(launch_p2p_wait(ctx->flags + hid, ep, ctx->p2p_timeout_ns, ctx->p2p_err_dev, ctx->stream));
+  if (w1) CK(cudaEventRecord(w1, ctx->stream));
   ++ctx->launches;
   float* src_acc = (float*)(ctx->peer_ws[a.owner] + ctx->peer_acc[a.owner][a.k]);
   for (int par = 0; par < 2; ++par) {
@@ -1355,6 +1380,9 @@ static ptycho_status appp_transport_setup(ptycho_ctx ctx) {
   for (int v : votes) all_ok &= v != 0;
   if (all_ok) {
     ctx->transport = PTYCHO_APPP_P2P;
+    CK(cudaHostAlloc((void**)&ctx->p2p_err, sizeof(unsigned), cudaHostAllocMapped));
+    *ctx->p2p_err = 0;
+    CK(cudaHostGetDevicePointer((void**)&ctx->p2p_err_dev, ctx->p2p_err, 0));
     return PTYCHO_OK;
   }
   for (void* m : ctx->peer_map) cudaIpcCloseMemHandle(m);
@@ -1475,6 +1503,59 @@ static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t co
   return join_tiles(ctx);
 }
 
+extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out) {
+  PASS(need_run(ctx));
+  if (!ms_out) return fail(ctx, PTYCHO_EARG, "ms_out is NULL");
+  CK(cudaSetDevice(ctx->device));
+  for (int i = 0; i < 5; ++i) ms_out[i] = 0.0;
+  size_t nmax = 0;
+  for (const Tile& t : ctx->tiles) nmax = std::max(nmax, t.probes.size());
+  if (nmax == 0) return PTYCHO_OK;
+  const int64_t T = ctx->cfg.pass_period > 0 ? ctx->cfg.pass_period : (int64_t)nmax;
+  const int64_t nseg = ((int64_t)nmax + T - 1) / T;
+  std::vector<cudaEvent_t> ev(4 * nseg + 1, nullptr), wait_ev;
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaEventRecord(ev[0], ctx->stream));
+  ptycho_status st = PTYCHO_OK;
+  ctx->wait_ev = &wait_ev;
+  for (int64_t j = 0; j < nseg && st == PTYCHO_OK; ++j) {
+    if (j) CK(cudaEventRecord(ev[4 * j], ctx->stream));
+    st = run_probes(ctx, j * T, T, CHAIN_GRAD);
+    if (st == PTYCHO_OK) st = cudaEventRecord(ev[4 * j + 1], ctx->stream) == cudaSuccess ? PTYCHO_OK : PTYCHO_ECUDA;
+    if (st == PTYCHO_OK) st = appp_range(ctx, 0, ctx->cfg.slices);
+    if (st == PTYCHO_OK) st = cudaEventRecord(ev[4 * j + 2], ctx->stream) == cudaSuccess ? PTYCHO_OK : PTYCHO_ECUDA;
+    if (st == PTYCHO_OK) st = step_range(ctx, 0, ctx->cfg.slices);
+    if (st == PTYCHO_OK) st = cudaEventRecord(ev[4 * j + 3], ctx->stream) == cudaSuccess ? PTYCHO_OK : PTYCHO_ECUDA;
+  }
+  ctx->wait_ev = nullptr;
+  if (st == PTYCHO_OK) {
+    CK(cudaEventRecord(ev[4 * nseg], ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    PASS(check_p2p(ctx));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[4 * nseg]));
+    ms_out[0] = ms;
+    double appp = 0.0;
+    for (int64_t j = 0; j < nseg; ++j) {
+      CK(cudaEventElapsedTime(&ms, ev[4 * j], ev[4 * j + 1]));
+      ms_out[1] += ms;
+      CK(cudaEventElapsedTime(&ms, ev[4 * j + 1], ev[4 * j + 2]));
+      appp += ms;
+      CK(cudaEventElapsedTime(&ms, ev[4 * j + 2], ev[4 * j + 3]));
+      ms_out[4] += ms;
+    }
+    for (size_t i = 0; i + 1 < wait_ev.size(); i += 2) {
+      CK(cudaEventElapsedTime(&ms, wait_ev[i], wait_ev[i + 1]));
+      ms_out[2] += ms;
+    }
+    ms_out[3] = std::max(0.0, appp - ms_out[2]);
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  for (auto e : wait_ev) cudaEventDestroy(e);
+  return st == PTYCHO_OK ? PTYCHO_OK : (ctx->err.empty() ? fail(ctx, st, "profile_iteration failed") : st);
+}
+
 extern "C" ptycho_status ptycho_iterate(ptycho_ctx ctx, double* loss_out) {
   PASS(need_run(ctx));
   CK(cudaSetDevice(ctx->device));
@@ -1547,6 +1628,15 @@ extern "C" ptycho_status ptycho_stitch(ptycho_ctx ctx, float* V_out, int out_on_
     if (am_root && !out_on_device) CK(cudaStreamSynchronize(ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  return check_p2p(ctx);
+}
+
+// A P2P flag wait that timed out (the peer stalled longer than PTYCHO_P2P_TIMEOUT_S) is reported
+// at the next synchronisation point; the AccBuf contents of that APPP call are then undefined.
+static ptycho_status check_p2p(ptycho_ctx ctx) {
+  if (ctx->p2p_err && *(volatile unsigned*)ctx->p2p_err)
+    return fail(ctx, PTYCHO_ECUDA, "APPP P2P: a peer did not reach its hop within %.0f s (PTYCHO_P2P_TIMEOUT_S)",
+                ctx->p2p_timeout_ns * 1e-9);
   return PTYCHO_OK;
 }
 
@@ -1557,7 +1647,7 @@ extern "C" ptycho_status ptycho_synchronize(ptycho_ctx ctx) {
   for (int k : ctx->local)
     if (ctx->tiles[k].stream) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
   if (ctx->copy_stream) CK(cudaStreamSynchronize(ctx->copy_stream));
-  return PTYCHO_OK;
+  return check_p2p(ctx);
 }
 
 extern "C" ptycho_status ptycho_kernel_launches(ptycho_ctx ctx, int64_t* count) {

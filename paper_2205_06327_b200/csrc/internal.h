@@ -103,8 +103,11 @@ cudaError_t launch_set_desc(int4* desc, const int2* centers, int v, int nk, int 
 cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t stream);
 cudaError_t launch_sum_double(const double* parts, int n, double* out, cudaStream_t stream);
 // APPP peer-to-peer transport: flag kernels (one thread each; see kernels.cu)
-cudaError_t launch_p2p_signal(unsigned* remote_ready, unsigned epoch, const unsigned* local_done, cudaStream_t s);
-cudaError_t launch_p2p_wait(const unsigned* local_ready, unsigned epoch, cudaStream_t s);
+// timeout_ns = 0: wait without limit; otherwise a timed-out wait sets *err (host-mapped) and returns
+cudaError_t launch_p2p_signal(unsigned* remote_ready, unsigned epoch, const unsigned* local_done,
+                              unsigned long long timeout_ns, unsigned* err, cudaStream_t s);
+cudaError_t launch_p2p_wait(const unsigned* local_ready, unsigned epoch, unsigned long long timeout_ns,
+                            unsigned* err, cudaStream_t s);
 cudaError_t launch_p2p_post(unsigned* remote_done, unsigned epoch, cudaStream_t s);
 
 }  // namespace ptycho

@@ -26,16 +26,42 @@
 namespace ptycho {
 
 // ------------------------------------------------------------------------------------------
-// complex helpers
+// complex helpers.  sm_100 packed FP32x2 (FADD2 / FMUL2 / FFMA2): one instruction updates both
+// halves of a complex64, and the operand modifiers of the packed forms (broadcast .F32, swap
+// .LO_HI, half negation .NP) absorb the swaps and sign flips of complex arithmetic, so a complex
+// add is 1 instruction (scalar: 2), a complex multiply 2 (scalar: 4) and a radix-4 butterfly 8
+// (scalar: 16).  The FP32 pipe time is the same (measured: FFMA2 issues at half the FFMA rate,
+// tools/ubench_f32x2.cu), but the passes are issue-bound, so the saved issue
+// slots are what counts.  Rounding is that of the scalar forms (each half is one RN add / mul /
+// fused multiply-add).  PTYCHO_SCALAR_FP builds the scalar arithmetic for A/B runs.
 // ------------------------------------------------------------------------------------------
+#ifndef PTYCHO_SCALAR_FP
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 csub_i(float2 a, float2 b) {  // a - i b
+  return __ffma2_rn(make_float2(b.y, b.x), make_float2(1.f, -1.f), a);
+}
+__device__ __forceinline__ float2 cadd_i(float2 a, float2 b) {  // a + i b
+  return __ffma2_rn(make_float2(b.y, b.x), make_float2(-1.f, 1.f), a);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {  // a*b = b.x a + b.y (-a.y, a.x)
+  return __ffma2_rn(make_float2(a.y, a.x), make_float2(-b.y, b.y), __fmul2_rn(make_float2(b.x, b.x), a));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b) = b.x a + b.y (a.y, -a.x)
+  return __ffma2_rn(make_float2(a.y, a.x), make_float2(b.y, -b.y), __fmul2_rn(make_float2(b.x, b.x), a));
+}
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 csub_i(float2 a, float2 b) { return make_float2(a.x + b.y, a.y - b.x); }
+__device__ __forceinline__ float2 cadd_i(float2 a, float2 b) { return make_float2(a.x - b.y, a.y + b.x); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
   return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
+#endif
 
 template <int P> struct Log2 { static constexpr int v = 1 + Log2<P / 2>::v; };
 template <> struct Log2<1> { static constexpr int v = 0; };
@@ -55,8 +81,7 @@ __device__ __forceinline__ float2 twmul32(float2 a, int m) {
   if (m == 8) return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
   if (m == 24) return INV ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
   const float c = tw_cos32(m), s = tw_sin32(m);
-  if (INV) return make_float2(a.x * c - a.y * s, a.x * s + a.y * c);
-  return make_float2(a.x * c + a.y * s, a.y * c - a.x * s);
+  return INV ? cmul(a, make_float2(c, s)) : cmul(a, make_float2(c, -s));
 }
 
 // In-register forward DFT of size P in {2,4,8,16,32}, natural order in and out, unnormalised
@@ -73,8 +98,8 @@ __device__ __forceinline__ void dft4(float2& a, float2& b, float2& c, float2& d)
   const float2 t0 = cadd(a, c), t1 = csub(a, c), t2 = cadd(b, d), t3 = csub(b, d);
   a = cadd(t0, t2);
   c = csub(t0, t2);
-  b = make_float2(t1.x + t3.y, t1.y - t3.x);  // t1 - i t3
-  d = make_float2(t1.x - t3.y, t1.y + t3.x);  // t1 + i t3
+  b = csub_i(t1, t3);
+  d = cadd_i(t1, t3);
 }
 
 template <int P> struct DftReg {
@@ -627,9 +652,14 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         }
         const float2 h = ht[m];
         const float2 y = x[k];
-        // conj(H) conj(y) = conj(H y) ;  H conj(y)
+        // conj(H) conj(y) = h.x conj(y) - h.y (y.y, y.x) ;  H conj(y) = h.x conj(y) + h.y (y.y, y.x)
+#ifndef PTYCHO_SCALAR_FP
+        const float hy = st == S_HC_FWD ? -h.y : h.y;
+        x[k] = __ffma2_rn(make_float2(y.y, y.x), make_float2(hy, hy), __fmul2_rn(make_float2(y.x, -y.y), make_float2(h.x, h.x)));
+#else
         if (st == S_HC_FWD) x[k] = make_float2(h.x * y.x - h.y * y.y, -(h.x * y.y + h.y * y.x));
         else x[k] = make_float2(h.x * y.x + h.y * y.y, h.y * y.x - h.x * y.y);
+#endif
       }
     } else if (has_step(PL, S_CONJ) && st == S_CONJ) {
 #pragma unroll
@@ -1303,7 +1333,11 @@ cudaError_t launch_sum_double(const double* parts, int n, double* out, cudaStrea
 // copies it in place -- no pack, no staging buffer, no NCCL.  One flag pair per hop orders the
 // two ranks: READY (sender -> receiver: the region is final) and DONE (receiver -> sender: the
 // region has been read, the sender may overwrite it).  Flags carry the APPP call's epoch, so they
-// never need resetting.  System-scope release/acquire; spins trap after 20 s instead of hanging.
+// never need resetting.  System-scope release/acquire.  A wait that exceeds timeout_ns (0 = no
+// limit; PTYCHO_P2P_TIMEOUT_S, default 600 s) does not trap: it raises *err (pinned host memory,
+// mapped) and returns, the host reports PTYCHO_ECUDA at its next synchronisation point, and the
+// peer's context stays usable (a trap poisons the context of a rank that merely waited
+// for a straggler).
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -1313,34 +1347,44 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void spin_until(const unsigned* flag, unsigned epoch) {
+__device__ __forceinline__ void spin_until(const unsigned* flag, unsigned epoch, unsigned long long timeout_ns,
+                                           unsigned* err) {
   const unsigned long long t0 = globaltimer();
   while ((int)(ld_acquire_sys(flag) - epoch) < 0) {
     __nanosleep(64);
-    if (globaltimer() - t0 > 20000000000ull) __trap();
+    if (timeout_ns && globaltimer() - t0 > timeout_ns) {
+      if (err) atomicExch_system(err, 1u);
+      return;
+    }
   }
 }
 
 // sender: publish "region final" to the receiver, then wait until the receiver has read it
-__global__ void p2p_signal_kernel(unsigned* remote_ready, unsigned epoch, const unsigned* local_done) {
+__global__ void p2p_signal_kernel(unsigned* remote_ready, unsigned epoch, const unsigned* local_done,
+                                  unsigned long long timeout_ns, unsigned* err) {
   __threadfence_system();  // AccBuf writes of the preceding kernels (stream order) before READY
   st_release_sys(remote_ready, epoch);
-  spin_until(local_done, epoch);
+  spin_until(local_done, epoch, timeout_ns, err);
 }
 // receiver: wait for READY (the copy kernel that follows on the stream then reads peer memory)
-__global__ void p2p_wait_kernel(const unsigned* local_ready, unsigned epoch) { spin_until(local_ready, epoch); }
+__global__ void p2p_wait_kernel(const unsigned* local_ready, unsigned epoch, unsigned long long timeout_ns,
+                                unsigned* err) {
+  spin_until(local_ready, epoch, timeout_ns, err);
+}
 // receiver: after the copy kernel, tell the sender its region may be overwritten
 __global__ void p2p_post_kernel(unsigned* remote_done, unsigned epoch) {
   __threadfence_system();
   st_release_sys(remote_done, epoch);
 }
 
-cudaError_t launch_p2p_signal(unsigned* remote_ready, unsigned epoch, const unsigned* local_done, cudaStream_t s) {
-  p2p_signal_kernel<<<1, 1, 0, s>>>(remote_ready, epoch, local_done);
+cudaError_t launch_p2p_signal(unsigned* remote_ready, unsigned epoch, const unsigned* local_done,
+                              unsigned long long timeout_ns, unsigned* err, cudaStream_t s) {
+  p2p_signal_kernel<<<1, 1, 0, s>>>(remote_ready, epoch, local_done, timeout_ns, err);
   return cudaGetLastError();
 }
-cudaError_t launch_p2p_wait(const unsigned* local_ready, unsigned epoch, cudaStream_t s) {
-  p2p_wait_kernel<<<1, 1, 0, s>>>(local_ready, epoch);
+cudaError_t launch_p2p_wait(const unsigned* local_ready, unsigned epoch, unsigned long long timeout_ns,
+                            unsigned* err, cudaStream_t s) {
+  p2p_wait_kernel<<<1, 1, 0, s>>>(local_ready, epoch, timeout_ns, err);
   return cudaGetLastError();
 }
 cudaError_t launch_p2p_post(unsigned* remote_done, unsigned epoch, cudaStream_t s) {

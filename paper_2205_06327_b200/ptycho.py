@@ -70,6 +70,7 @@ _SIGS = {
     "ptycho_synchronize": [_P],
     "ptycho_kernel_launches": [_P, _c.POINTER(_c.c_int64)],
     "ptycho_profile_chain": [_P, _c.c_int32, _c.c_int64, _c.c_int64, _P, _P],
+    "ptycho_profile_iteration": [_P, _P],
     "ptycho_debug_read_tile": [_P, _c.c_int32, _c.c_int32, _P],
     "ptycho_debug_write_tile": [_P, _c.c_int32, _c.c_int32, _P],
     "ptycho_debug_probe_grad": [_P, _c.c_int32, _c.c_int64, _P, _c.POINTER(_c.c_double)],
@@ -122,13 +123,36 @@ def _ptr(a):
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.flags["C_CONTIGUOUS"]
         return a.ctypes.data
     return a.data_ptr()
 
 
 def _on_device(a):
     return 0 if (a is None or isinstance(a, np.ndarray)) else int(a.is_cuda)
+
+
+_KIND = {"f32": (np.float32, "float32"), "c64": (np.complex64, "complex64")}
+
+
+def _check(a, kind, count, device, what):
+    """Validate a buffer handed to the C ABI: dtype, C-contiguity, element count, and for CUDA
+    tensors the context's device.  The library trusts sizes, so a wrong buffer would otherwise be
+    read or written out of bounds (EARG instead)."""
+    if a is None:
+        return
+    npt, tname = _KIND[kind]
+    if isinstance(a, np.ndarray):
+        ok_type, contig, numel = a.dtype == npt, a.flags["C_CONTIGUOUS"], a.size
+    else:
+        ok_type, contig, numel = str(a.dtype) == "torch." + tname, a.is_contiguous(), a.numel()
+        if a.is_cuda and a.device.index != device:
+            raise PtychoError(1, f"{what}: tensor on cuda:{a.device.index}, context on cuda:{device}")
+    if not ok_type:
+        raise PtychoError(1, f"{what}: dtype {a.dtype}, expected {tname}")
+    if not contig:
+        raise PtychoError(1, f"{what}: not C-contiguous")
+    if count is not None and numel != count:
+        raise PtychoError(1, f"{what}: {numel} elements, expected {count}")
 
 
 class Ptycho:
@@ -156,9 +180,14 @@ class Ptycho:
             raise PtychoError(st, lib.ptycho_last_error(self.h).decode())
 
     def close(self):
+        """Wait for every queued library kernel (tile, copy and context streams), then destroy the
+        context, and only then release the workspace to PyTorch's caching allocator (a kernel still
+        in flight must never see its memory handed to another tensor)."""
         if getattr(self, "h", None):
-            lib.ptycho_destroy(self.h)
+            lib.ptycho_synchronize(self.h)
+            lib.ptycho_destroy(self.h)  # also synchronizes (and fences the P2P peers)
             self.h = None
+        self.workspace = None
 
     def __del__(self):
         try:
@@ -222,11 +251,13 @@ class Ptycho:
     def set_probe(self, probe):
         if isinstance(probe, np.ndarray):
             probe = np.ascontiguousarray(probe, dtype=np.complex64)
+        _check(probe, "c64", self.cfg.n ** 2, self.device, "probe")
         self._ck(lib.ptycho_set_probe(self.h, _ptr(probe), _on_device(probe)))
 
     def load_measurements(self, amp, first_local=0, flags=0):
         if isinstance(amp, np.ndarray):
             amp = np.ascontiguousarray(amp, dtype=np.float32)
+        _check(amp, "f32", len(amp) * self.cfg.n ** 2, self.device, "measurements")
         self._ck(lib.ptycho_load_measurements(self.h, _ptr(amp), _on_device(amp), first_local, len(amp), flags))
 
     def read_measurements(self, first_local=0, count=None, out=None):
@@ -235,12 +266,17 @@ class Ptycho:
         n = self.cfg.n
         if out is None:
             out = np.zeros((count, n, n), np.float32)
+        _check(out, "f32", count * n * n, self.device, "read_measurements out")
+        if not isinstance(out, np.ndarray) and out.is_cuda:
+            raise PtychoError(1, "read_measurements writes host memory: pass a numpy array or a CPU tensor")
         self._ck(lib.ptycho_read_measurements(self.h, _ptr(out), first_local, count))
         return out
 
     def set_volume(self, volume=None):
         if isinstance(volume, np.ndarray):
             volume = np.ascontiguousarray(volume, dtype=np.float32)
+        c = self.cfg
+        _check(volume, "f32", c.slices * c.height * c.width, self.device, "volume")
         self._ck(lib.ptycho_set_volume(self.h, _ptr(volume), _on_device(volume)))
 
     def simulate_measurements(self):
@@ -275,6 +311,7 @@ class Ptycho:
         c = self.cfg
         if out is None and rank == root:
             out = np.zeros((c.slices, c.height, c.width), np.float32)
+        _check(out, "f32", c.slices * c.height * c.width, self.device, "stitch out")
         self._ck(lib.ptycho_stitch(self.h, _ptr(out), _on_device(out), root))
         return out
 
@@ -295,6 +332,12 @@ class Ptycho:
         cnt = np.zeros(len(self.PASS_KINDS), np.int64)
         self._ck(lib.ptycho_profile_chain(self.h, tile, first, count, ms.ctypes.data, cnt.ctypes.data))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.PASS_KINDS) if cnt[i]}
+
+    def profile_iteration(self):
+        """One real iteration with serial phases; per-phase ms on this rank (collective)."""
+        ms = np.zeros(5, np.float64)
+        self._ck(lib.ptycho_profile_iteration(self.h, ms.ctypes.data))
+        return dict(zip(["total_ms", "compute_ms", "wait_ms", "comm_ms", "acc_step_ms"], (float(v) for v in ms)))
 
     # ---- debug exports
     def debug_read_tile(self, tile, which):
@@ -324,6 +367,7 @@ class Ptycho:
         """d f_i / d V over the full window of GLOBAL probe `probe` (host numpy or device tensor out)."""
         n, s = self.cfg.n, self.cfg.slices
         g = np.zeros((s, n, n), np.float32) if out is None else out
+        _check(g, "f32", s * n * n, self.device, "probe_grad out")
         loss = ctypes.c_double()
         self._ck(lib.ptycho_probe_grad(self.h, probe, _ptr(g), ctypes.byref(loss)))
         return g, loss.value
@@ -331,5 +375,6 @@ class Ptycho:
     def probe_exitwave(self, probe, out=None):
         n = self.cfg.n
         psi = np.zeros((n, n), np.complex64) if out is None else out
+        _check(psi, "c64", n * n, self.device, "probe_exitwave out")
         self._ck(lib.ptycho_probe_exitwave(self.h, probe, _ptr(psi)))
         return psi
