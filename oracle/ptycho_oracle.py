@@ -22,6 +22,11 @@ Parity status of each function (all pinned; see tests/test_oracle_pins.py):
   appp_passes .......... coverage count (all ones), random-int global sum, negative control
   reconstruct .......... K=1 literal SGD, alpha=0 frozen equivalence (north_star invariant)
   stitch ............... round trip
+  hve_decompose ........ SPEC worked example (3x3 mesh, 3x3 scan, one extra row -> centre tile holds all 9),
+                         1x1 trivial case, TileTooSmall predicate by brute force
+  hve_reconstruct ...... 1x1 == plain per-probe SGD, all-probes-everywhere == single tile, halos == owners'
+                         interiors bitwise after every exchange
+  seam_score ........... closed forms (constant field -> 0 jumps; a step placed on a tile border)
 The paper's Tables II/III cannot be reproduced (no dataset, no Summit): parity unpinned
 for those, and they are not computed here.
 """
@@ -479,3 +484,127 @@ def accumulate_frozen(v0, probe, amps, centers, cfg, rows, cols, halo, tau=TAU):
             _scatter(accs[k], t["ext"], (cy, cx), n, g, window_mask(t["ext"], (cy, cx), n), 1.0)
     appp_passes(accs, tiles, rows, cols)
     return accs, tiles
+
+
+# ---------------------------------------------------------------------------------
+# Halo Voxel Exchange (HVE) baseline -- the paper's comparison system
+#   P:344-369 (§Related Work): tiles get "additional probe locations that are neighbors",
+#   halos "augmented accordingly to cover all the additional circles", independent tile
+#   reconstructions, then "the voxels in each tile are pasted to the halos in neighboring GPUs",
+#   repeated until convergence; "two extra rows of probe locations for each tile".
+#   Readings (DESIGN.md §2 #33-#36): extra rows = a margin of (rows x scan step) pixels around the
+#   interior; the augmented rect is the bounding box of the interior and every assigned window,
+#   clipped to the object; one sweep of per-probe SGD per tile per iteration, then the copy-paste.
+# ---------------------------------------------------------------------------------
+class TileTooSmall(ValueError):
+    """a tile's augmented halo reaches past its adjacent tiles' interiors (the paper's
+    'NA' entries: each tile must be large enough to hold its neighbours' halos)."""
+
+
+def hve_decompose(height: int, width: int, rows: int, cols: int, centers, n: int, margin: int):
+    """Tiles with interior (uniform split, reading #14), probes = every probe whose centre lies in
+    the interior dilated by `margin` pixels (own + extra rows, ascending global index), and the
+    augmented rect = bounding box of the interior and those probes' N x N windows, clipped to the
+    object.  Raises TileTooSmall if an augmented rect extends past the interiors of the tile's
+    row/column neighbours (copy-paste could not fill that halo from an adjacent tile)."""
+    ys = split_extent(height, rows)
+    xs = split_extent(width, cols)
+    tiles = []
+    for r in range(rows):
+        for c in range(cols):
+            y0, y1 = ys[r]
+            x0, x1 = xs[c]
+            probes = [i for i, (cy, cx) in enumerate(centers)
+                      if y0 - margin <= cy < y1 + margin and x0 - margin <= cx < x1 + margin]
+            ay0, ax0, ay1, ax1 = y0, x0, y1, x1
+            for i in probes:
+                cy, cx = int(centers[i][0]), int(centers[i][1])
+                ay0, ax0 = min(ay0, cy - n // 2), min(ax0, cx - n // 2)
+                ay1, ax1 = max(ay1, cy - n // 2 + n), max(ax1, cx - n // 2 + n)
+            aug = (max(0, ay0), max(0, ax0), min(height, ay1), min(width, ax1))
+            lo_y = ys[r - 1][0] if r > 0 else 0
+            hi_y = ys[r + 1][1] if r + 1 < rows else height
+            lo_x = xs[c - 1][0] if c > 0 else 0
+            hi_x = xs[c + 1][1] if c + 1 < cols else width
+            if aug[0] < lo_y or aug[2] > hi_y or aug[1] < lo_x or aug[3] > hi_x:
+                raise TileTooSmall(f"tile ({r},{c}): augmented rect {aug} reaches past its neighbours' interiors")
+            tiles.append(dict(r=r, c=c, interior=(y0, x0, y1, x1), ext=aug, probes=probes))
+    return tiles
+
+
+def hve_exchange(vks, tiles):
+    """Copy-paste (REPLACE): every tile's halo voxels take the value of the tile whose interior
+    holds them ("the voxels in each tile are pasted to the halos in neighboring GPUs").
+    Interiors partition the object, so each halo voxel has exactly one writer.  Returns the number
+    of (source, destination) messages."""
+    msgs = 0
+    snap = [v.copy() for v in vks]  # interiors as they were after the sweep (synchronous exchange)
+    for j, tj in enumerate(tiles):
+        for k, tk in enumerate(tiles):
+            if k == j:
+                continue
+            y0 = max(tj["ext"][0], tk["interior"][0])
+            y1 = min(tj["ext"][2], tk["interior"][2])
+            x0 = max(tj["ext"][1], tk["interior"][1])
+            x1 = min(tj["ext"][3], tk["interior"][3])
+            if y0 < y1 and x0 < x1:
+                _region_views(vks[j], tj["ext"], (y0, y1), (x0, x1))[...] = \
+                    _region_views(snap[k], tk["ext"], (y0, y1), (x0, x1))
+                msgs += 1
+    return msgs
+
+
+def hve_reconstruct(v0, probe, amps, centers, cfg, rows, cols, margin, iterations, alpha, tau=TAU):
+    """HVE: per iteration, every tile independently runs one sweep of per-probe SGD
+    (g = d f_i / d V, V[win ^ aug] -= alpha g, probes ascending) over its own + extra probes on its
+    augmented tile, then the synchronous copy-paste exchange; finally stitch the interiors.
+    Returns (V [S][H][W], [F per iteration: sum over every tile's probes, duplicates included], vks)."""
+    n, sigma, c = cfg["n"], cfg["sigma"], cfg["prop_c"]
+    slices, height, width = v0.shape
+    tiles = hve_decompose(height, width, rows, cols, centers, n, margin)
+    vks = decompose(v0, tiles)
+    losses = []
+    for _ in range(iterations):
+        total = 0.0
+        for k, t in enumerate(tiles):
+            for i in t["probes"]:
+                cy, cx = int(centers[i][0]), int(centers[i][1])
+                g, f = probe_grad(probe, window(vks[k], t["ext"], (cy, cx), n), amps[i], sigma, c, tau)
+                total += f
+                _scatter(vks[k], t["ext"], (cy, cx), n, g, window_mask(t["ext"], (cy, cx), n), -alpha)
+        hve_exchange(vks, tiles)
+        losses.append(total)
+    return stitch(vks, tiles, slices, height, width), losses, vks
+
+
+def seam_score(err, height: int, width: int, rows: int, cols: int) -> float:
+    """Seam artifacts (Fig. artifact; SPEC SeamScore): mean |jump| of the error field
+    err = V_rec - V_true across tile borders, divided by its mean |jump| between neighbouring voxels
+    elsewhere.  ~1: no seam; > 1: discontinuities at the borders."""
+    ys = [a for a, _ in split_extent(height, rows)][1:]
+    xs = [a for a, _ in split_extent(width, cols)][1:]
+    dy = np.abs(np.diff(err, axis=1))  # jump between rows y-1 and y at index y-1
+    dx = np.abs(np.diff(err, axis=2))
+    by = np.zeros(dy.shape[1], bool)
+    bx = np.zeros(dx.shape[2], bool)
+    for y in ys:
+        by[y - 1] = True
+    for x in xs:
+        bx[x - 1] = True
+    border = np.concatenate([dy[:, by, :].ravel(), dx[:, :, bx].ravel()])
+    inner = np.concatenate([dy[:, ~by, :].ravel(), dx[:, :, ~bx].ravel()])
+    if border.size == 0 or inner.mean() == 0:
+        return 0.0
+    return float(border.mean() / inner.mean())
+
+
+def memory_report(tiles, slices: int, n: int):
+    """Analytic per-tile storage (SPEC memory_report): voxels of the (extended / augmented) rect x S
+    and measurement values (assigned probes x N^2)."""
+    out = []
+    for t in tiles:
+        y0, x0, y1, x1 = t["ext"]
+        nprobe = len(t["probes"]) if "probes" in t else None
+        out.append(dict(voxels=(y1 - y0) * (x1 - x0) * slices,
+                        measurements=None if nprobe is None else nprobe * n * n))
+    return out

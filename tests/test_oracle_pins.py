@@ -563,3 +563,82 @@ def test_reconstruct_multi_tile_segments_hand_composed():
     expect = O.stitch(vks, tiles, s, h, w)
     out, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 2, 1, n // 2, 1, alpha=a, alpha_acc=aa, period=T)
     assert rel(out - v0, expect - v0) < 1e-10
+
+
+# ----------------------------------------------------------------------------- HVE baseline
+def test_hve_spec_example_centre_tile_holds_all_nine():
+    # SPEC S:480 / P:360-362 (Fig. halo_voxel_exch1 d-e): 3x3 mesh, 3x3 scan, one extra row of
+    # probe locations -> the corner tile holds 4 probes, an edge tile 6, the centre tile all 9
+    centers = synth.scan_centers(96, 96, 3, 3)          # centres 16, 48, 80: step 32
+    tiles = O.hve_decompose(96, 96, 3, 3, centers, 16, margin=32)
+    counts = [len(t["probes"]) for t in tiles]
+    assert counts == [4, 6, 4, 6, 9, 6, 4, 6, 4]
+    assert tiles[4]["probes"] == list(range(9))
+    # augmented rect = bbox of the interior and the assigned 16 x 16 windows
+    assert tiles[4]["ext"] == (8, 8, 88, 88)
+    assert tiles[0]["ext"] == (0, 0, 56, 56)
+
+
+def test_hve_trivial_mesh_and_too_small_tiles():
+    centers = synth.scan_centers(96, 96, 6, 6)
+    t = O.hve_decompose(96, 96, 1, 1, centers, 16, margin=16)
+    assert len(t) == 1 and t[0]["probes"] == list(range(36)) and t[0]["ext"] == (0, 0, 96, 96)
+    with pytest.raises(O.TileTooSmall):
+        O.hve_decompose(96, 96, 6, 6, centers, 16, margin=32)  # interiors 16 < halo reach
+    O.hve_decompose(96, 96, 3, 3, centers, 16, margin=16)      # interiors 32: fine
+
+
+def _hve_problem(seed=41):
+    n, s, h, w = 16, 2, 48, 48
+    rng = np.random.default_rng(seed)
+    p = synth.probe(n, 3.0, aperture_frac=0.3)
+    vt = rng.random((s, h, w))
+    centers = synth.scan_centers(h, w, 6, 6)  # step 8
+    cfg = dict(n=n, sigma=0.3, prop_c=1.0)
+    amps = [O.farfield_magnitude(p, O.window(vt, (0, 0, h, w), tuple(c), n), 0.3, 1.0) for c in centers]
+    return p, vt, centers, cfg, amps
+
+
+def test_hve_one_tile_is_plain_sgd():
+    # 1x1: HVE is sequential per-probe SGD, i.e. Alg. 1 on one tile without the accumulated step
+    p, vt, centers, cfg, amps = _hve_problem()
+    v0 = 0.5 * vt
+    a, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 1, 1, 8, 2, alpha=2.0)
+    b, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 2, alpha=2.0, alpha_acc=0.0)
+    assert np.array_equal(a, b)
+
+
+def test_hve_all_probes_everywhere_equals_single_tile():
+    # with every probe on every tile (2x2 mesh, margin past the object) each tile runs the
+    # full reconstruction on the whole object -> the exchange is a no-op and the stitch equals 1x1
+    p, vt, centers, cfg, amps = _hve_problem()
+    v0 = 0.5 * vt
+    tiles = O.hve_decompose(48, 48, 2, 2, centers, 16, margin=100)
+    assert all(len(t["probes"]) == 36 and t["ext"] == (0, 0, 48, 48) for t in tiles)
+    a, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 2, 2, 100, 2, alpha=2.0)
+    b, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 2, alpha=2.0)
+    assert np.array_equal(a, b)
+
+
+def test_hve_halos_equal_owner_interiors_after_exchange():
+    # after each copy-paste every halo voxel equals its owner's interior voxel bitwise
+    p, vt, centers, cfg, amps = _hve_problem()
+    v0 = 0.5 * vt
+    out, _, vks = O.hve_reconstruct(v0, p, amps, centers, cfg, 2, 2, 8, 1, alpha=2.0)
+    tiles = O.hve_decompose(48, 48, 2, 2, centers, 16, margin=8)
+    for vk, t in zip(vks, tiles):
+        y0, x0, y1, x1 = t["ext"]
+        assert np.array_equal(vk, out[:, y0:y1, x0:x1])  # every voxel of R_k = the stitched (owner) value
+    # and the result differs from GD's (the methods are not equivalent with partial probe sets)
+    gd, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 2, 2, 8, 1, alpha=2.0, alpha_acc=0.0)
+    assert not np.array_equal(out, gd)
+
+
+def test_seam_score_closed_form():
+    s, h, w, xb = 2, 10, 12, 6  # 1x2 mesh: one vertical border between x = 5 and x = 6
+    a, b = 0.5, 3.0
+    xx = np.arange(w)[None, None, :] * np.ones((s, h, 1))
+    err = a * xx + b * (xx >= xb)
+    inner_mean = a * s * h * (w - 2) / (s * (h - 1) * w + s * h * (w - 2))
+    assert abs(O.seam_score(err, h, w, 1, 2) - (a + b) / inner_mean) < 1e-12
+    assert O.seam_score(np.ones((s, h, w)), h, w, 2, 2) == 0.0
