@@ -119,6 +119,19 @@ ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t cols, int32
                                const int32_t* tile_owner, const void* nccl_id, int32_t rank,
                                int32_t nranks);
 
+/* Halo Voxel Exchange baseline (the paper's comparison system; "two extra rows
+ * of probe locations ... halo width of 890 Picometers"), instead of set_tiles.
+ * Same grid and R_k = interior dilated by `halo`; set_scan assigns to tile k EVERY probe whose
+ * centre lies in its interior dilated by `margin` px (own + extra rows: margin = rows x scan
+ * step), so a probe may sit on several tiles (local_probes lists the duplicates).  iterate =
+ * one per-probe SGD sweep per tile (steps 6, 8; no AccBuf, passes or accumulated step), then the
+ * copy-paste: every halo voxel is REPLACED by the tile whose interior holds it.
+ * appp_passes = the exchange alone; step is ESTATE; cross-rank messages use NCCL.  A halo wider
+ * than the adjacent interiors (the paper's "NA") is EHALO.  Collective like set_tiles. */
+ptycho_status ptycho_set_tiles_hve(ptycho_ctx ctx, int32_t rows, int32_t cols, int32_t halo, int32_t margin,
+                                   const int32_t* tile_owner, const void* nccl_id, int32_t rank,
+                                   int32_t nranks);
+
 /* Host-only geometry (no context, no GPU): rects[8*k .. 8*k+8) = {ext y0,x0,y1,x1, interior
  * y0,x0,y1,x1} of tile k = r*C + c for the grid set_tiles would build (same code). */
 ptycho_status ptycho_tile_geometry(int32_t height, int32_t width, int32_t rows, int32_t cols, int32_t halo,

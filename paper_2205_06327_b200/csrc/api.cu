@@ -27,6 +27,7 @@ struct Hop {       // one APPP message: dst (op)= src on region [y0,y1) x [x0,x1
   int src, dst;
   int y0, y1, x0, x1;
   int add;         // 1 = ADD (forward passes), 0 = REPLACE (backward passes)
+  int vol = 0;     // 0: AccBuf (APPP); 1: V (HVE copy-paste exchange)
 };
 
 struct Tile {
@@ -119,6 +120,8 @@ struct ptycho_ctx_s {
   bool use_pdl = true;
   int slab = 0;  // slices per APPP slab in ptycho_iterate (0 = passes after the whole segment)
   bool persist = false;  // run probe chains in the persistent cooperative chain kernel
+  bool hve = false;      // Halo Voxel Exchange baseline (ptycho_set_tiles_hve)
+  int hve_margin = 0;    // HVE probe-assignment margin (pixels)
   bool batched = false;  // opt-in batched schedule (non-overlapping windows side by side)
   int batch = 1;         // batch slots per tile
   // APPP transport between ranks (decided, collectively, at the first APPP call)
@@ -419,6 +422,39 @@ extern "C" ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t 
   return PTYCHO_OK;
 }
 
+// HVE baseline: GD's grid and halo rects, no APPP hops; set_scan assigns duplicates and
+// builds the copy-paste list.  Cross-rank exchange messages go over NCCL.
+extern "C" ptycho_status ptycho_set_tiles_hve(ptycho_ctx ctx, int32_t rows, int32_t cols, int32_t halo,
+                                              int32_t margin, const int32_t* tile_owner, const void* nccl_id,
+                                              int32_t rank, int32_t nranks) {
+  if (!ctx) return PTYCHO_EARG;
+  if (margin < 0) return fail(ctx, PTYCHO_EARG, "margin %d < 0", margin);
+  PASS(ptycho_set_tiles(ctx, rows, cols, halo, tile_owner, nccl_id, rank, nranks));
+  ctx->hve = true;
+  ctx->hve_margin = margin;
+  ctx->hops.clear();
+  ctx->transport_req = PTYCHO_APPP_NCCL;
+  // TileTooSmall: each halo must lie inside the adjacent tiles' interiors
+  for (const Tile& t : ctx->tiles) {
+    const Tile& up = ctx->tiles[std::max(0, t.r - 1) * cols + t.c];
+    const Tile& dn = ctx->tiles[std::min(rows - 1, t.r + 1) * cols + t.c];
+    const Tile& lf = ctx->tiles[t.r * cols + std::max(0, t.c - 1)];
+    const Tile& rt = ctx->tiles[t.r * cols + std::min(cols - 1, t.c + 1)];
+    if (t.ey0 < up.iy0 || t.ey1 > dn.iy1 || t.ex0 < lf.ix0 || t.ex1 > rt.ix1)
+      return fail(ctx, PTYCHO_EHALO, "HVE: tile %d's halo %d reaches past its neighbours' interiors (tile too small)",
+                  t.k, halo);
+  }
+  // copy-paste list: tile j's halo voxels inside tile k's interior <- tile k (every pair, k != j)
+  for (const Tile& j : ctx->tiles)
+    for (const Tile& k : ctx->tiles) {
+      if (k.k == j.k) continue;
+      Hop h{k.k, j.k, std::max(j.ey0, k.iy0), std::min(j.ey1, k.iy1), std::max(j.ex0, k.ix0), std::min(j.ex1, k.ix1), 0};
+      h.vol = 1;
+      if (h.y0 < h.y1 && h.x0 < h.x1) ctx->hops.push_back(h);
+    }
+  return PTYCHO_OK;
+}
+
 extern "C" ptycho_status ptycho_set_scan(ptycho_ctx ctx, const int32_t* centers_yx, int64_t n_probes) {
   if (!ctx) return PTYCHO_EARG;
   if (!ctx->tiles_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles must precede set_scan");
@@ -432,6 +468,12 @@ extern "C" ptycho_status ptycho_set_scan(ptycho_ctx ctx, const int32_t* centers_
     if (cy < 0 || cy >= cfg.height || cx < 0 || cx >= cfg.width)
       return fail(ctx, PTYCHO_EARG, "probe %lld centre (%d,%d) outside the %dx%d object", (long long)i, cy, cx,
                   cfg.height, cfg.width);
+    if (ctx->hve) {  // every tile whose interior dilated by the margin holds the centre
+      const int m = ctx->hve_margin;
+      for (Tile& t : ctx->tiles)
+        if (cy >= t.iy0 - m && cy < t.iy1 + m && cx >= t.ix0 - m && cx < t.ix1 + m) t.probes.push_back(i);
+      continue;
+    }
     // centre containment in half-open interiors (reading #15): row/column by the uniform split
     const int base_y = cfg.height / ctx->R, base_x = cfg.width / ctx->C;
     const int r = std::min(cy / base_y, ctx->R - 1), c = std::min(cx / base_x, ctx->C - 1);
@@ -522,7 +564,7 @@ static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
     Tile& t = ctx->tiles[k];
     const size_t vol = (size_t)t.slice_stride * S;
     t.V = (float*)take(vol * sizeof(float));
-    t.acc = (float*)take(vol * sizeof(float));
+    t.acc = ctx->hve ? nullptr : (float*)take(vol * sizeof(float));  // HVE keeps no AccBuf
     const size_t B = (size_t)ctx->batch;
     t.stash = (float2*)take(B * stash_slices(cfg) * n2 * sizeof(float2));
     t.wf[0] = (float2*)take(B * n2 * sizeof(float2));
@@ -553,7 +595,7 @@ static ptycho_status zero_tiles(ptycho_ctx ctx, bool v, bool a) {
     Tile& t = ctx->tiles[k];
     const size_t vol = (size_t)t.slice_stride * ctx->cfg.slices;
     if (v) CK(cudaMemsetAsync(t.V, 0, vol * sizeof(float), ctx->stream));
-    if (a) CK(cudaMemsetAsync(t.acc, 0, vol * sizeof(float), ctx->stream));
+    if (a && t.acc) CK(cudaMemsetAsync(t.acc, 0, vol * sizeof(float), ctx->stream));
   }
   return PTYCHO_OK;
 }
@@ -888,6 +930,7 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   a.stash_slot = (long long)stash_slices(ctx->cfg) * ctx->cfg.n * ctx->cfg.n;
   a.stash_store = 1;
   a.wf_slot = (long long)ctx->cfg.n * ctx->cfg.n;
+  a.no_acc = ctx->hve ? 1 : 0;
   return a;
 }
 
@@ -1222,8 +1265,8 @@ static ptycho_status hop_local(ptycho_ctx ctx, const Hop& h, int z0, int z1) {
   const Tile& a = ctx->tiles[h.src];
   const Tile& b = ctx->tiles[h.dst];
   for (int par = 0; par < 2; ++par) {
-    SliceView vs = region_view(a, a.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
-    SliceView vd = region_view(b, b.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    SliceView vs = region_view(a, h.vol ? a.V : a.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    SliceView vd = region_view(b, h.vol ? b.V : b.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
     if (vs.nslices == 0) continue;
     CK(launch_copy2d(vd.base, vd.ld, vd.ss, vs.base, vs.ld, vs.ss, vs.rows, vs.cols, vs.nslices, h.add, ctx->stream));
     ++ctx->launches;
@@ -1239,7 +1282,7 @@ static ptycho_status hop_remote(ptycho_ctx ctx, const Hop& h, bool sender, int z
   const size_t area = (size_t)(h.y1 - h.y0) * (h.x1 - h.x0);
   const int slab = (int)std::max<size_t>(1, ctx->msg_floats / area);
   for (int par = 0; par < 2; ++par) {
-    SliceView v = region_view(me, me.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
+    SliceView v = region_view(me, h.vol ? me.V : me.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
     for (int q0 = 0; q0 < v.nslices; q0 += slab) {
       const int nz = std::min(slab, v.nslices - q0);
       const size_t cnt = area * nz;
@@ -1441,6 +1484,7 @@ extern "C" ptycho_status ptycho_appp_passes(ptycho_ctx ctx) {
 
 extern "C" ptycho_status ptycho_step(ptycho_ctx ctx) {
   PASS(need_ws(ctx));
+  if (ctx->hve) return fail(ctx, PTYCHO_ESTATE, "HVE has no accumulated step (Alg. 1 steps 14-16 are GD's)");
   CK(cudaSetDevice(ctx->device));
   return step_range(ctx, 0, ctx->cfg.slices);
 }
@@ -1506,6 +1550,7 @@ static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t co
 extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out) {
   PASS(need_run(ctx));
   if (!ms_out) return fail(ctx, PTYCHO_EARG, "ms_out is NULL");
+  if (ctx->hve) return fail(ctx, PTYCHO_ESTATE, "profile_iteration: GD contexts only");
   CK(cudaSetDevice(ctx->device));
   for (int i = 0; i < 5; ++i) ms_out[i] = 0.0;
   size_t nmax = 0;
@@ -1565,7 +1610,11 @@ extern "C" ptycho_status ptycho_iterate(ptycho_ctx ctx, double* loss_out) {
   const int64_t T = ctx->cfg.pass_period > 0 ? ctx->cfg.pass_period : (int64_t)nmax;
   const int64_t nseg = ((int64_t)nmax + T - 1) / T;
   if (loss_out) PASS(zero_loss(ctx));
-  for (int64_t j = 0; j < nseg; ++j) {
+  if (ctx->hve) {  // HVE: one independent SGD sweep per tile, then the copy-paste exchange
+    PASS(run_probes(ctx, 0, (int64_t)nmax, CHAIN_GRAD));
+    PASS(appp_range(ctx, 0, ctx->cfg.slices));
+  }
+  for (int64_t j = 0; j < nseg && !ctx->hve; ++j) {
     if (ctx->slab > 0) {
       PASS(segment_pipelined(ctx, j * T, T));
     } else {
@@ -1675,6 +1724,7 @@ extern "C" ptycho_status ptycho_debug_read_tile(ptycho_ctx ctx, int32_t tile, in
   CK(cudaStreamSynchronize(ctx->stream));
   for (int k : ctx->local) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
   const float* buf = which ? t->acc : t->V;
+  if (!buf) return fail(ctx, PTYCHO_EARG, "tile %d has no AccBuf (HVE context)", tile);
   const size_t area = (size_t)t->eh * t->ew;
   for (int s = 0; s < ctx->cfg.slices; ++s) {
     // staging viewed as [eh][ew]: use a private pitch = ew by calling the kernels directly
@@ -1696,6 +1746,7 @@ extern "C" ptycho_status ptycho_debug_write_tile(ptycho_ctx ctx, int32_t tile, i
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   float* buf = which ? t->acc : t->V;
+  if (!buf) return fail(ctx, PTYCHO_EARG, "tile %d has no AccBuf (HVE context)", tile);
   const size_t area = (size_t)t->eh * t->ew;
   for (int s = 0; s < ctx->cfg.slices; ++s) {
     float* sl = buf + (long long)s * t->slice_stride;

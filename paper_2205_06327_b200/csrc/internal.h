@@ -43,6 +43,7 @@ struct PassArgs {
   int batch;                // probes processed side by side (batched schedule; 1 = sequential)
   long long stash_slot;     // float2 between the stashes of consecutive batch slots
   long long wf_slot;        // float2 between the wavefields of consecutive batch slots
+  int no_acc;               // HVE baseline: per-probe SGD only, AccBuf neither read nor written
 };
 
 enum PassKind : int {

@@ -597,7 +597,9 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       const int j = q + Q * k, p = LL.pos0 + j;
       if (LL.ok && (unsigned)p < (unsigned)LL.plim) {
         cp_async4s(pv + j, vrow + p, pol);
-        if constexpr (kind_grad(KIND)) cp_async4s(pacc + j, arow + p, pol);
+        if constexpr (kind_grad(KIND)) {
+          if (!a.no_acc) cp_async4s(pacc + j, arow + p, pol);
+        }
       } else {
         pv[j] = 0.f;
         if constexpr (kind_grad(KIND)) pacc[j] = 0.f;
@@ -773,7 +775,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
         const float v = pv[j];
         if (!exporting && (unsigned)p < (unsigned)lim) {
-          st_stream(arow + p, pacc[j] + g, pol);
+          if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
           st_stream(vrow + p, v - a.alpha * g, pol);
         }
         pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
@@ -794,7 +796,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
         const float v = pv[j];
         if (!exporting && (unsigned)p < (unsigned)lim) {
-          arow[p] = pacc[j] + g;
+          if (!a.no_acc) arow[p] = pacc[j] + g;
           vrow[p] = v - a.alpha * g;
         }
         pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export

@@ -45,6 +45,7 @@ _SIGS = {
     "ptycho_destroy": [_P],
     "ptycho_nccl_unique_id": [_P, _c.c_size_t],
     "ptycho_set_tiles": [_P, _c.c_int32, _c.c_int32, _c.c_int32, _P, _P, _c.c_int32, _c.c_int32],
+    "ptycho_set_tiles_hve": [_P, _c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _P, _P, _c.c_int32, _c.c_int32],
     "ptycho_set_scan": [_P, _P, _c.c_int64],
     "ptycho_tile_geometry": [_c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _P],
     "ptycho_appp_schedule": [_c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _c.c_int32, _P, _c.c_int32,
@@ -208,6 +209,15 @@ class Ptycho:
         nid = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
         self._own = own
         self._ck(lib.ptycho_set_tiles(self.h, rows, cols, halo, _ptr(own), nid, rank, nranks))
+        self.rows, self.cols = rows, cols
+
+    def set_tiles_hve(self, rows, cols, halo, margin, tile_owner=None, nccl_id=None, rank=0, nranks=1):
+        """Halo Voxel Exchange baseline: probes within `margin` px of a tile's interior
+        are duplicated onto it; iterate = independent SGD sweeps + halo copy-paste."""
+        own = None if tile_owner is None else np.ascontiguousarray(tile_owner, dtype=np.int32)
+        nid = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
+        self._own = own
+        self._ck(lib.ptycho_set_tiles_hve(self.h, rows, cols, halo, margin, _ptr(own), nid, rank, nranks))
         self.rows, self.cols = rows, cols
 
     def set_scan(self, centers):

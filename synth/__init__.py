@@ -19,7 +19,7 @@ from __future__ import annotations
 import dataclasses
 import numpy as np
 
-__all__ = ["Config", "CONFIGS", "volume", "probe", "scan_centers", "random_amplitudes"]
+__all__ = ["Config", "CONFIGS", "volume", "probe", "scan_centers", "random_amplitudes", "lattice_phantom"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -80,3 +80,29 @@ def random_amplitudes(seed: int, count: int, n: int, scale: float = 1.0) -> np.n
     """Non-negative float32 amplitudes [count][N][N] (DC at [0,0]) with the RMS of a unit probe."""
     rng = np.random.default_rng(seed)
     return (rng.random((count, n, n), dtype=np.float32) * (2.0 * scale / n)).astype(np.float32)
+
+
+def lattice_phantom(seed: int, slices: int, height: int, width: int, period: float = 39.0, sigma_px: float = 6.0,
+                    amplitude: float = 1.0, jitter: float = 1.5) -> np.ndarray:
+    """Structured potential for the seam / quality studies only (SPEC make_phantom
+    S:523-531): a PbTiO3-like square lattice of Gaussian atom columns, period ~3.9 A = 39 px at
+    10 pm/px ("each circle ... a small group of atoms"), seeded positional jitter, values
+    in [0, amplitude], float32 [S][H][W]."""
+    rng = np.random.default_rng(seed)
+    out = np.zeros((slices, height, width), np.float64)
+    yy = np.arange(height)[:, None]
+    xx = np.arange(width)[None, :]
+    cys = np.arange(period / 2, height, period)
+    cxs = np.arange(period / 2, width, period)
+    for s in range(slices):
+        acc = np.zeros((height, width))
+        for cy in cys:
+            for cx in cxs:
+                jy, jx = rng.normal(0.0, jitter, 2)
+                y0, x0 = cy + jy, cx + jx
+                ys = slice(max(0, int(y0 - 4 * sigma_px)), min(height, int(y0 + 4 * sigma_px) + 1))
+                xs = slice(max(0, int(x0 - 4 * sigma_px)), min(width, int(x0 + 4 * sigma_px) + 1))
+                acc[ys, xs] += np.exp(-((yy[ys] - y0) ** 2 + (xx[:, xs] - x0) ** 2) / (2 * sigma_px ** 2))
+        out[s] = acc
+    out *= amplitude / max(out.max(), 1e-30)
+    return out.astype(np.float32)
