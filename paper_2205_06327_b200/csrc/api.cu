@@ -65,6 +65,7 @@ struct Tile {
     int64_t begin;
     cudaEvent_t ev;
   };
+  CUtensorMap tmV[2], tmA[2];            // TMA descriptors of V / AccBuf per slice parity
   std::vector<AmpChunk> amp_pend;
   size_t amp_cur = 0;
   std::vector<cudaEvent_t> amp_pool;
@@ -600,6 +601,35 @@ static ptycho_status zero_tiles(ptycho_ctx ctx, bool v, bool a) {
   return PTYCHO_OK;
 }
 
+// TMA descriptors: slice parity p of a tile buffer as a 3-D tensor
+// {position along the line, line, slice / 2} with the layout's row pitch and 2 slice strides;
+// box = one line segment of min(N, 256) floats.  OOB: zero fill (loads) / clipped (stores).
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static ptycho_status make_tensor_maps(ptycho_ctx ctx, const Tile& t, float* buf, CUtensorMap out[2]) {
+  static EncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        !encode)
+      return fail(ctx, PTYCHO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  }
+  const int S = ctx->cfg.slices, n = ctx->cfg.n;
+  const cuuint32_t box[3] = {(cuuint32_t)std::min(n, 256), 1, 1}, es[3] = {1, 1, 1};
+  for (int par = 0; par < 2; ++par) {
+    const cuuint64_t nz = (cuuint64_t)std::max(1, par == 0 ? (S + 1) / 2 : S / 2);
+    const cuuint64_t dims[3] = {(cuuint64_t)(par == 0 ? t.ew : t.eh), (cuuint64_t)(par == 0 ? t.eh : t.ew), nz};
+    const cuuint64_t strides[2] = {(cuuint64_t)(par == 0 ? t.pitch0 : t.pitch1) * 4, (cuuint64_t)t.slice_stride * 8};
+    float* base = buf + (par == 0 ? 0 : (S > 1 ? t.slice_stride : 0));
+    const CUresult r = encode(&out[par], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ctx, PTYCHO_ECUDA, "cuTensorMapEncodeTiled(tile %d, parity %d): error %d", t.k, par, (int)r);
+  }
+  return PTYCHO_OK;
+}
+
 extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_dev, size_t bytes) {
   if (!ctx) return PTYCHO_EARG;
   if (!ctx->tiles_set || !ctx->scan_set) return fail(ctx, PTYCHO_ESTATE, "set_tiles and set_scan first");
@@ -617,6 +647,9 @@ extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_de
   CK(cudaMemcpyAsync(ctx->htab, ctx->h_htab.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
   for (int k : ctx->local) {
     Tile& t = ctx->tiles[k];
+    PASS(make_tensor_maps(ctx, t, t.V, t.tmV));
+    if (t.acc) PASS(make_tensor_maps(ctx, t, t.acc, t.tmA));
+    else memcpy(t.tmA, t.tmV, sizeof t.tmA);  // HVE: never dereferenced (no_acc)
     std::vector<int2> hc(std::max<size_t>(t.probes.size(), 1), make_int2(0, 0));
     for (size_t j = 0; j < t.probes.size(); ++j)
       hc[j] = make_int2(ctx->centers[2 * t.probes[j]], ctx->centers[2 * t.probes[j] + 1]);
@@ -949,6 +982,8 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
   auto go = [&](PassKind kind, int s, bool last) -> ptycho_status {
     PassArgs b = a;
     b.s = s;
+    b.tmV = t.tmV[s & 1];
+    b.tmA = t.tmA[s & 1];
     const bool recon = kind == K_RECON_FIRST || kind == K_RECON_MID || kind == K_RECON_END;
     b.stash_s = ring ? (s & 1) : s;
     // stash-free: the forward keeps only phi_{S-1}; the phi chain recomputes the others
@@ -1648,8 +1683,36 @@ extern "C" ptycho_status ptycho_stitch(ptycho_ctx ctx, float* V_out, int out_on_
   CK(cudaSetDevice(ctx->device));
   const auto& cfg = ctx->cfg;
   const size_t hw = (size_t)cfg.height * cfg.width;
+  // A pinned host V_out (cudaHostAlloc / registered, e.g. torch pin_memory) is written in place by
+  // the gather kernels through its device alias (zero-copy): no staging, no per-slice sync.
+  float* host_dev = nullptr;
+  if (am_root && !out_on_device) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, V_out) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+      host_dev = (float*)at.devicePointer;
+    cudaGetLastError();
+  }
+  float* gout = out_on_device ? V_out : host_dev;
+  if (ctx->nranks == 1 && gout) {
+    // every tile local: one gather per tile and slice parity (even slices copy, odd transpose)
+    for (const Tile& t : ctx->tiles)
+      for (int par = 0; par < 2; ++par) {
+        SliceView v = region_view(t, t.V, par, 0, cfg.slices, t.iy0, t.iy1, t.ix0, t.ix1);
+        if (v.nslices == 0) continue;
+        float* dst = gout + (size_t)par * hw + (size_t)t.iy0 * cfg.width + t.ix0;
+        if (par == 0)
+          CK(launch_copy2d(dst, cfg.width, 2 * (long long)hw, v.base, v.ld, v.ss, v.rows, v.cols, v.nslices, 0,
+                           ctx->stream));
+        else
+          CK(launch_transpose2d(dst, cfg.width, 2 * (long long)hw, v.base, v.ld, v.ss, t.iy1 - t.iy0, t.ix1 - t.ix0,
+                                v.nslices, 0, ctx->stream));
+        ++ctx->launches;
+      }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return check_p2p(ctx);
+  }
   for (int s = 0; s < cfg.slices; ++s) {
-    float* g = am_root ? (out_on_device ? V_out + (size_t)s * hw : ctx->staging) : nullptr;
+    float* g = am_root ? (gout ? gout + (size_t)s * hw : ctx->staging) : nullptr;
     for (const Tile& t : ctx->tiles) {
       const int ih = t.iy1 - t.iy0, iw = t.ix1 - t.ix0;
       if (t.owner == ctx->rank && am_root) {
@@ -1672,9 +1735,10 @@ extern "C" ptycho_status ptycho_stitch(ptycho_ctx ctx, float* V_out, int out_on_
         ++ctx->launches;
       }
     }
-    if (am_root && !out_on_device)
+    if (am_root && !gout) {
       CK(cudaMemcpyAsync(V_out + (size_t)s * hw, ctx->staging, hw * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-    if (am_root && !out_on_device) CK(cudaStreamSynchronize(ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return check_p2p(ctx);

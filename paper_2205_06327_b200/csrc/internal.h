@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cstddef>
+#include <cuda.h>  // CUtensorMap (TMA descriptors of V_k / AccBuf_k)
 #include <cuda_runtime.h>
 
 namespace ptycho {
@@ -44,6 +45,11 @@ struct PassArgs {
   long long stash_slot;     // float2 between the stashes of consecutive batch slots
   long long wf_slot;        // float2 between the wavefields of consecutive batch slots
   int no_acc;               // HVE baseline: per-probe SGD only, AccBuf neither read nor written
+  // TMA descriptors of V_k and AccBuf_k for this pass's slice parity (3-D: position along the
+  // line, line, slice/2; box = min(N, 256) positions of one line; out-of-bounds = zero fill on
+  // load, clipped on store -- exactly the zero-extension of reading #12 and the win ^ R_k mask).
+  // Read by the kernels from the __grid_constant__ parameter; unused by the persistent chain.
+  CUtensorMap tmV, tmA;
 };
 
 enum PassKind : int {

@@ -132,19 +132,22 @@ template <> struct DftReg<4> {
   __device__ __forceinline__ static void run(float2 (&x)[4]) { dft4(x[0], x[1], x[2], x[3]); }
 };
 
-// exp(i x) for the transmission t = exp(i sigma V): Cephes minimax polynomials on |x| <= pi/4
-// (about 1 ulp, no range reduction -- sigma V is a small phase for any physical potential),
-// sincospi with its exact reduction otherwise.
+// exp(i x) for the transmission t = exp(i sigma V): Cephes minimax polynomials (about 1 ulp) on
+// the reduced argument r = x - k pi/2, k = rint(2x/pi) (two-constant Cody-Waite reduction, exact
+// for the |k| a phase sigma V can reach), quadrant by k mod 4.  Branch-free: the earlier
+// warp-vote fast path (|x| <= pi/4) split every unrolled element of the pointwise loops into its
+// own basic block; for |x| <= pi/4, k = 0 and the result is bit-identical to it.
 __device__ __forceinline__ void sincos_t(float x, float* sn, float* cs) {
-  // warp-uniform branch: a per-lane branch gets if-converted and evaluates both paths
-  if (__all_sync(0xffffffffu, fabsf(x) <= 0.785398163f)) {
-    const float z = x * x;
-    *sn = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * x, x);
-    *cs = fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f), z * z,
-               fmaf(-0.5f, z, 1.0f));
-  } else {
-    sincospif(x * 0.318309886183790672f, sn, cs);
-  }
+  const float k = rintf(x * 0.636619772367581343f);
+  const float r = fmaf(k, 4.37113900018624283e-8f, fmaf(-k, 1.57079637050628662f, x));  // pi/2 = hi - 4.37e-8
+  const float z = r * r;
+  const float s0 = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * r, r);
+  const float c0 = fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f),
+                        z * z, fmaf(-0.5f, z, 1.0f));
+  const int q = (int)k;
+  const float s1 = (q & 1) ? c0 : s0, c1 = (q & 1) ? s0 : c0;
+  *sn = (q & 2) ? -s1 : s1;
+  *cs = ((q + 1) & 2) ? -c1 : c1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -490,6 +493,40 @@ __device__ __forceinline__ void st_stream(float2* p, float2 v, unsigned long lon
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// ---- TMA (cp.async.bulk.tensor) and bulk copies with an mbarrier (one per CTA, used once)
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE;\n"
+      " bra LAB_WAIT;\n DONE:\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                          unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(z),
+      "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap* map, int x, int y, int z, const void* src,
+                                           unsigned long long pol) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
+               ::"l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(src)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                          unsigned long long pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Location of this line inside R_k for slice parity ax.
 struct LineLoc {
   long long row;  // offset of (line, pos=0) in the slice, valid only if ok
@@ -524,7 +561,8 @@ struct Smem {
   static constexpr bool TW_REG = (ENG::T * ENG::T == N);               // twiddles in registers
   static constexpr size_t tw = 0;                                    // twiddles (engine layout)
   static constexpr size_t ht = tw + (TW_REG ? 0 : (size_t)ENG::TW * 8);  // H_1/N, m = 0..N/2
-  static constexpr size_t lines = ht + (N / 2 + 2) * 8;
+  static constexpr size_t bar = ht + (N / 2 + 2) * 8;                // mbarrier of the TMA prefetch
+  static constexpr size_t lines = (bar + 8 + 127) / 128 * 128;       // per-line buffers, 128-B aligned (TMA)
   static constexpr size_t ex_b = (size_t)ENG::EX * 8;                // exchange buffer per line
   static constexpr size_t st_b = kind_grad(KIND) ? (size_t)N * 8 : 0;  // stash prefetch per line
   static constexpr size_t v_b =
@@ -533,7 +571,12 @@ struct Smem {
   static constexpr size_t per_line = ex_b + st_b + v_b + acc_b;
   static constexpr size_t stage_b = (size_t)N * (L + 1) * 8;         // transposed-store staging
   static constexpr size_t total = lines + (per_line * L > stage_b ? per_line * L : stage_b);
+  static constexpr size_t alloc = total + 128;  // dynamic smem is aligned to 128 B at run time
 };
+__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
+  return (unsigned char*)(((uintptr_t)p + 127) & ~(uintptr_t)127);
+}
+__host__ __device__ constexpr int tma_box(int n) { return n < 256 ? n : 256; }
 
 // The body of one pass for one group of LINES_PER_CTA lines (grp).  PERSIST = false: a
 // standalone kernel in a CUDA-graph/PDL chain (tables loaded here, probe from *desc, input read
@@ -544,7 +587,8 @@ template <int N, int KIND, bool PERSIST, bool TWG = false>
 __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4 pd,
                                           const float2 (&twr)[EngOf<N>::type::T * EngOf<N>::type::T == N
                                                                   ? EngOf<N>::type::E : 1],
-                                          unsigned char* smem) {
+                                          unsigned char* smem, const CUtensorMap* tmV = nullptr,
+                                          const CUtensorMap* tmA = nullptr) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
   constexpr Plan PL = plan_of(KIND);
@@ -588,7 +632,49 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   const int i = pd.x, wy0 = pd.y, wx0 = pd.z;
   const int ax = a.s & 1;
   LineLoc LL = line_loc(a, ax, line, wy0, wx0);
-  if constexpr (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND)) {
+  // TMA path (standalone pass kernels): one thread loads every line's V / AccBuf row segments as
+  // 1-D boxes of the 3-D tensor maps (out-of-bounds = zero fill: reading #12 for free) and the
+  // stash / |y| rows as bulk copies, all on one mbarrier; the updated V / AccBuf rows go back as
+  // TMA stores clipped to R_k.  The persistent chain keeps per-element cp.async.
+#ifdef PTYCHO_NO_TMA
+  constexpr bool TMA = false;  // A/B build: per-element cp.async prefetch and st.global write-back
+#else
+  constexpr bool TMA = !PERSIST;
+#endif
+  constexpr int BOX = tma_box(N), NBOX = N / BOX;
+  constexpr bool NEED_V = kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND);
+  unsigned long long* mbar = (unsigned long long*)(smem + SM::bar);
+  // line index inside the slice layout and window position 0 along the line (tile coordinates)
+  const int lidx = ax == 0 ? wy0 + line - a.ey0 : wx0 + line - a.ex0;
+  const int pos0 = LL.pos0;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar, 1);
+      fence_proxy_async();
+      constexpr unsigned per = (NEED_V ? 4u * N : 0u) + (kind_grad(KIND) ? 8u * N : 0u) + (KIND == K_TURN ? 4u * N : 0u);
+      const unsigned acc_bytes = (kind_grad(KIND) && !a.no_acc) ? 4u * N : 0u;
+      mbar_expect_tx(mbar, (per + acc_bytes) * L);
+      for (int l = 0; l < L; ++l) {
+        const int ln = grp * L + l;
+        const int li = ax == 0 ? wy0 + ln - a.ey0 : wx0 + ln - a.ex0;
+        unsigned char* lb = smem + SM::lines + l * SM::per_line;
+        if constexpr (NEED_V) {
+#pragma unroll
+          for (int b = 0; b < NBOX; ++b) tma_load3(lb + SM::ex_b + SM::st_b + b * BOX * 4, tmV, pos0 + b * BOX, li, a.s >> 1, mbar, pol);
+        }
+        if constexpr (kind_grad(KIND)) {
+          if (!a.no_acc) {
+#pragma unroll
+            for (int b = 0; b < NBOX; ++b)
+              tma_load3(lb + SM::ex_b + SM::st_b + SM::v_b + b * BOX * 4, tmA, pos0 + b * BOX, li, a.s >> 1, mbar, pol);
+          }
+          bulk_load(lb + SM::ex_b, a.stash + (size_t)a.stash_s * N * N + (size_t)ln * N, 8u * N, mbar, pol);
+        }
+        if constexpr (KIND == K_TURN) bulk_load(lb + SM::ex_b + SM::st_b, a.amp + (size_t)i * N * N + (size_t)ln * N, 4u * N, mbar, pol);
+      }
+    }
+  }
+  if constexpr (!TMA && (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND))) {
     const long long so = (long long)a.s * a.slice_stride + LL.row;
     const float* vrow = a.V + so;
     const float* arow = a.acc + so;
@@ -606,19 +692,24 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       }
     }
   }
-  if constexpr (kind_grad(KIND)) {
+  if constexpr (!TMA && kind_grad(KIND)) {
     const float4* src = (const float4*)(a.stash + (size_t)a.stash_s * N * N + (size_t)line * N);
     float4* dst = (float4*)pst;
 #pragma unroll 4
     for (int c = q; c < N / 2; c += Q) cp_async16s(dst + c, src + c, pol);
   }
-  if constexpr (KIND == K_TURN) {
+  if constexpr (!TMA && KIND == K_TURN) {
     const float4* src = (const float4*)(a.amp + (size_t)i * N * N + (size_t)line * N);
     float4* dst = (float4*)pv;
 #pragma unroll 4
     for (int c = q; c < N / 4; c += Q) cp_async16s(dst + c, src + c, pol);
   }
   cp_async_commit();
+  // the row prefetches have landed (all threads; before any read of pst / pv / pacc)
+  auto prefetch_wait = [&]() {
+    if constexpr (TMA) mbar_wait(mbar, 0);
+    else cp_async_wait_all();
+  };
   float2 x[P];
   if constexpr (FIRST) {
     const float2* src = a.probe + (size_t)line * N + q;
@@ -635,7 +726,8 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = __ldcg(src + Q * k);
   }
-  asm volatile("cp.async.wait_group 1;" ::: "memory");  // tables landed (row prefetches may not have)
+  if constexpr (TMA) cp_async_wait_all();  // tables landed (the TMA rows are tracked by the mbarrier)
+  else asm volatile("cp.async.wait_group 1;" ::: "memory");  // tables landed (row prefetches may not have)
   __syncthreads();
 
   float part = 0.f;  // loss partial (RESID)
@@ -668,7 +760,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       for (int k = 0; k < P; ++k) x[k].y = -x[k].y;
     } else if (has_step(PL, S_TRANSMIT) && st == S_TRANSMIT) {
       // phi_s = exp(i sigma V_s[win ^ R_k]) psi_s  (t = 1 outside R_k, reading #12); stash phi_s
-      cp_async_wait_all();
+      prefetch_wait();
       float2* stp = a.stash + (size_t)a.stash_s * N * N + (size_t)line * N + q;
       const bool keep = a.stash_store != 0;  // stash-free: only phi_{S-1} is kept
 #ifndef PTYCHO_UNROLLED_STEPS
@@ -702,7 +794,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 #endif
     } else if (has_step(PL, S_RESID) && st == S_RESID) {
       // X = raw 2-D DFT (N x true F phi_{S-1}); |Psi| = |X|/N (App. A: |H| = 1)
-      cp_async_wait_all();
+      prefetch_wait();
       ENG::sync_line(bid);
       const float invn = 1.0f / (float)N;
 #pragma unroll
@@ -725,7 +817,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       // stash-free adjoint: phi_s (conj pending after P^H, or true from the stash) -> stash ring
       // slot; psi_s = conj(t_s) phi_s with t_s from the pre-update V (the gradient pass of slice
       // s runs after this one).  Rolled through the idle exchange buffer like S_GRAD.
-      cp_async_wait_all();
+      prefetch_wait();
       ENG::sync_line(bid);
       float2* stp = a.stash + (size_t)a.stash_s * N * N + (size_t)line * N;
       const bool pending = (st == S_RECON);
@@ -753,7 +845,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       const long long so = (long long)a.s * a.slice_stride + LL.row;
       float* vrow = a.V + so;
       float* arow = a.acc + so;
-      cp_async_wait_all();
+      prefetch_wait();
       ENG::sync_line(bid);
       const float two_sigma = 2.0f * a.sigma;
       const bool exporting = a.gexport != nullptr;  // debug: write g instead of updating
@@ -774,17 +866,42 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         const float2 chi = make_float2(y.x, -y.y);
         const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
         const float v = pv[j];
-        if (!exporting && (unsigned)p < (unsigned)lim) {
-          if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
-          st_stream(vrow + p, v - a.alpha * g, pol);
+        if constexpr (TMA) {
+          // updated rows in place; written back below as TMA stores clipped to R_k
+          if (!exporting) {
+            pacc[j] += g;
+            pv[j] = v - a.alpha * g;
+          } else {
+            pacc[j] = g;  // debug export of g; V / AccBuf untouched
+          }
+        } else {
+          if (!exporting && (unsigned)p < (unsigned)lim) {
+            if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
+            st_stream(vrow + p, v - a.alpha * g, pol);
+          }
+          pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
         }
-        pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
         float sn, cs;
         sincos_t(a.sigma * v, &sn, &cs);
         xs[j] = cmulc(chi, make_float2(cs, sn));
       }
 #pragma unroll
       for (int k = 0; k < P; ++k) x[k] = xs[ENG::idx(dist, q, k)];
+      if constexpr (TMA) {
+        if (!exporting) {  // Alg. 1 steps 7-8 write-back: V and AccBuf rows of win ^ R_k
+          fence_proxy_async();  // this thread's st.shared -> visible to the async proxy
+          ENG::sync_line(bid);
+          if (q == 0) {
+#pragma unroll
+            for (int b = 0; b < NBOX; ++b) tma_store3(tmV, pos0 + b * BOX, lidx, a.s >> 1, pv + b * BOX, pol);
+            if (!a.no_acc) {
+#pragma unroll
+              for (int b = 0; b < NBOX; ++b) tma_store3(tmA, pos0 + b * BOX, lidx, a.s >> 1, pacc + b * BOX, pol);
+            }
+            bulk_commit();
+          }
+        }
+      }
 #else
 #pragma unroll
       for (int k = 0; k < P; ++k) {
@@ -853,6 +970,11 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     for (int k = 0; k < P; ++k) x[k].y = -x[k].y;
   }
   constexpr int STORE = kind_store(KIND);
+  // the TMA write-back of this CTA's V / AccBuf rows has read shared memory before it is reused
+  // (the staging area overlaps the line buffers)
+  if constexpr (TMA && kind_grad(KIND)) {
+    if (q == 0) bulk_wait_read();
+  }
   if constexpr (STORE == 1) {
     // out[j][line]: stage the CTA's L = 4 lines as 32-B rows [j][4] (element l stored at
     // l ^ ((j >> 2) & 3): conflict-free column writes), then write 16-B chunks of each output
@@ -884,6 +1006,9 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     }
   }
 
+  if constexpr (TMA && kind_grad(KIND)) {
+    if (q == 0) bulk_wait();  // V / AccBuf rows in global memory before the CTA retires
+  }
   if (!PERSIST && a.advance) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -907,12 +1032,13 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 // passes always use 2 (they spill at 168).  Both builds execute the same arithmetic.
 template <int N, int KIND, int MINB>
 __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KIND) ? 2 : MINB)
-pass_kernel(const PassArgs a) {
+pass_kernel(const __grid_constant__ PassArgs a) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T;
   constexpr bool TWG = MINB >= 4 && !kind_grad(KIND) && ENG::T * ENG::T == N;
   constexpr bool TW_REG = (ENG::T * ENG::T == N) && !TWG;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = align128(smem_raw);
   const int q = threadIdx.x % Q;
   // four-step engines keep the thread's twiddles in registers (no shared-memory table)
   float2 twr[ENG::T * ENG::T == N ? P : 1];
@@ -924,8 +1050,9 @@ pass_kernel(const PassArgs a) {
   // probe descriptor and loss partials)
   constexpr int groups = N / LINES_PER_CTA;
   const int b = blockIdx.x / groups, grp = blockIdx.x - b * groups;
+  // the tensor maps are used in place in the __grid_constant__ parameter (param-space address)
   if (b == 0) {
-    pass_body<N, KIND, false, TWG>(a, grp, make_int4(0, 0, 0, 0), twr, smem);
+    pass_body<N, KIND, false, TWG>(a, grp, make_int4(0, 0, 0, 0), twr, smem, &a.tmV, &a.tmA);
   } else {
     PassArgs ab = a;
     ab.stash += b * a.stash_slot;
@@ -933,7 +1060,7 @@ pass_kernel(const PassArgs a) {
     ab.out += b * a.wf_slot;
     ab.desc += b;
     ab.loss_part += b * groups;
-    pass_body<N, KIND, false, TWG>(ab, grp, make_int4(0, 0, 0, 0), twr, smem);
+    pass_body<N, KIND, false, TWG>(ab, grp, make_int4(0, 0, 0, 0), twr, smem, &a.tmV, &a.tmA);
   }
 }
 
@@ -986,7 +1113,8 @@ __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2) chain_ker
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
   constexpr bool TW_REG = (ENG::T * ENG::T == N);
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = align128(smem_raw);
   const int q = threadIdx.x % Q;
   float2 twr[TW_REG ? P : 1];
   if constexpr (TW_REG) {
@@ -1037,9 +1165,9 @@ __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2) chain_ker
 template <int N>
 static size_t chain_smem() {
   size_t m = 0;
-  const size_t v[] = {Smem<N, K_FWD_FIRST_PROP>::total, Smem<N, K_FWD_FIRST_FFT>::total, Smem<N, K_FWD_MID>::total,
-                      Smem<N, K_FWD_LAST>::total,       Smem<N, K_TURN>::total,          Smem<N, K_BWD_LAST_PROP>::total,
-                      Smem<N, K_BWD_LAST_END>::total,   Smem<N, K_BWD_MID>::total,       Smem<N, K_BWD_END>::total};
+  const size_t v[] = {Smem<N, K_FWD_FIRST_PROP>::alloc, Smem<N, K_FWD_FIRST_FFT>::alloc, Smem<N, K_FWD_MID>::alloc,
+                      Smem<N, K_FWD_LAST>::alloc,       Smem<N, K_TURN>::alloc,          Smem<N, K_BWD_LAST_PROP>::alloc,
+                      Smem<N, K_BWD_LAST_END>::alloc,   Smem<N, K_BWD_MID>::alloc,       Smem<N, K_BWD_END>::alloc};
   for (size_t x : v) m = x > m ? x : m;
   return m;
 }
@@ -1076,7 +1204,7 @@ cudaError_t launch_chain(int n, const ChainArgs& c, cudaStream_t stream) {
 template <int N, int KIND, int MINB>
 static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) {
   auto kern = pass_kernel<N, KIND, MINB>;
-  const size_t smem = Smem<N, KIND>::total;
+  const size_t smem = Smem<N, KIND>::alloc;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

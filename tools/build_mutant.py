@@ -16,8 +16,8 @@ sys.path.insert(0, os.path.join(ROOT, "paper_2205_06327_b200"))
 import build as B  # noqa: E402
 
 MUTANTS = {
-    "no_v_step": ("st_stream(vrow + p, v - a.alpha * g, pol);", "(void)vrow;"),
-    "flip_v_step": ("st_stream(vrow + p, v - a.alpha * g, pol);", "st_stream(vrow + p, v + a.alpha * g, pol);"),
+    "no_v_step": ("pv[j] = v - a.alpha * g;", "(void)0;"),
+    "flip_v_step": ("pv[j] = v - a.alpha * g;", "pv[j] = v + a.alpha * g;"),
 }
 
 
