@@ -65,7 +65,7 @@ struct Tile {
     int64_t begin;
     cudaEvent_t ev;
   };
-  CUtensorMap tmV[2], tmA[2];            // TMA descriptors of V / AccBuf per slice parity
+  CUtensorMap* tm_dev = nullptr;  // TMA descriptors, device copies: [V 0, V 1, A 0, A 1] main box, + 4 tail box
   std::vector<AmpChunk> amp_pend;
   size_t amp_cur = 0;
   std::vector<cudaEvent_t> amp_pool;
@@ -119,6 +119,7 @@ struct ptycho_ctx_s {
   cudaEvent_t ev_fork = nullptr;
   bool use_graph = true;
   bool use_pdl = true;
+  bool debug_sync = false;  // PTYCHO_DEBUG_SYNC: synchronize after every direct pass launch
   int slab = 0;  // slices per APPP slab in ptycho_iterate (0 = passes after the whole segment)
   bool persist = false;  // run probe chains in the persistent cooperative chain kernel
   bool hve = false;      // Halo Voxel Exchange baseline (ptycho_set_tiles_hve)
@@ -201,6 +202,7 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   ctx->stream = (cudaStream_t)cuda_stream;
   if (const char* e = getenv("PTYCHO_NO_GRAPH")) ctx->use_graph = atoi(e) == 0;
   if (const char* e = getenv("PTYCHO_NO_PDL")) ctx->use_pdl = atoi(e) == 0;
+  if (const char* e = getenv("PTYCHO_DEBUG_SYNC")) ctx->debug_sync = atoi(e) != 0;
   // APPP slab size: ~S/10 slices (>= 1); PTYCHO_SLAB overrides, 0 disables the pipelining
   ctx->slab = std::max(1, (cfg->slices + 9) / 10);
   if (const char* e = getenv("PTYCHO_SLAB")) ctx->slab = std::max(0, atoi(e));
@@ -578,6 +580,7 @@ static size_t plan_workspace(ptycho_ctx ctx, bool carve) {
     t.amp = (float*)take(std::max<size_t>(t.probes.size(), 1) * n2 * sizeof(float));
     t.centers = (int2*)take(std::max<size_t>(t.probes.size(), 1) * sizeof(int2));
     t.desc = (int4*)take(B * sizeof(int4));
+    t.tm_dev = (CUtensorMap*)take(8 * sizeof(CUtensorMap));
     t.done = (unsigned*)take(sizeof(unsigned));
     t.loss_part = (double*)take(B * (n / LINES_PER_CTA) * sizeof(double));
   }
@@ -607,7 +610,7 @@ static ptycho_status zero_tiles(ptycho_ctx ctx, bool v, bool a) {
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static ptycho_status make_tensor_maps(ptycho_ctx ctx, const Tile& t, float* buf, CUtensorMap out[2]) {
+static ptycho_status make_tensor_maps(ptycho_ctx ctx, const Tile& t, float* buf, CUtensorMap out[2], int box0) {
   static EncodeTiled encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -616,7 +619,8 @@ static ptycho_status make_tensor_maps(ptycho_ctx ctx, const Tile& t, float* buf,
       return fail(ctx, PTYCHO_ECUDA, "cuTensorMapEncodeTiled unavailable");
   }
   const int S = ctx->cfg.slices, n = ctx->cfg.n;
-  const cuuint32_t box[3] = {(cuuint32_t)std::min(n, 256), 1, 1}, es[3] = {1, 1, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)box0, 1, 1}, es[3] = {1, 1, 1};
+  (void)n;
   for (int par = 0; par < 2; ++par) {
     const cuuint64_t nz = (cuuint64_t)std::max(1, par == 0 ? (S + 1) / 2 : S / 2);
     const cuuint64_t dims[3] = {(cuuint64_t)(par == 0 ? t.ew : t.eh), (cuuint64_t)(par == 0 ? t.eh : t.ew), nz};
@@ -647,9 +651,18 @@ extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_de
   CK(cudaMemcpyAsync(ctx->htab, ctx->h_htab.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
   for (int k : ctx->local) {
     Tile& t = ctx->tiles[k];
-    PASS(make_tensor_maps(ctx, t, t.V, t.tmV));
-    if (t.acc) PASS(make_tensor_maps(ctx, t, t.acc, t.tmA));
-    else memcpy(t.tmA, t.tmV, sizeof t.tmA);  // HVE: never dereferenced (no_acc)
+#ifndef PTYCHO_TMA_BOX
+#define PTYCHO_TMA_BOX 256
+#endif
+    // main box = min(N, 256) floats (kernels.cu tma_box), tail box = 4 floats (16 B); AccBuf maps
+    // alias V's in HVE contexts (no AccBuf, never dereferenced)
+    CUtensorMap h[8];
+    const int bmain = std::min((int)n, PTYCHO_TMA_BOX);
+    PASS(make_tensor_maps(ctx, t, t.V, h + 0, bmain));
+    PASS(make_tensor_maps(ctx, t, t.acc ? t.acc : t.V, h + 2, bmain));
+    PASS(make_tensor_maps(ctx, t, t.V, h + 4, 4));
+    PASS(make_tensor_maps(ctx, t, t.acc ? t.acc : t.V, h + 6, 4));
+    CK(cudaMemcpy(t.tm_dev, h, sizeof h, cudaMemcpyHostToDevice));
     std::vector<int2> hc(std::max<size_t>(t.probes.size(), 1), make_int2(0, 0));
     for (size_t j = 0; j < t.probes.size(); ++j)
       hc[j] = make_int2(ctx->centers[2 * t.probes[j]], ctx->centers[2 * t.probes[j] + 1]);
@@ -982,8 +995,8 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
   auto go = [&](PassKind kind, int s, bool last) -> ptycho_status {
     PassArgs b = a;
     b.s = s;
-    b.tmV = t.tmV[s & 1];
-    b.tmA = t.tmA[s & 1];
+    b.tmV = t.tm_dev + (s & 1);
+    b.tmA = t.tm_dev + 2 + (s & 1);
     const bool recon = kind == K_RECON_FIRST || kind == K_RECON_MID || kind == K_RECON_END;
     b.stash_s = ring ? (s & 1) : s;
     // stash-free: the forward keeps only phi_{S-1}; the phi chain recomputes the others
@@ -1014,6 +1027,10 @@ static ptycho_status enqueue_chain(ptycho_ctx ctx, Tile& t, ChainMode mode, cuda
       prof->kind.push_back((int)kind);
     } else {
       CK(launch_pass(n, kind, b, st, ctx->use_pdl));
+      if (ctx->debug_sync) {  // PTYCHO_DEBUG_SYNC=1: name the pass that faults (not during capture)
+        const cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(ctx, PTYCHO_ECUDA, "pass kind %d slice %d: %s", (int)kind, s, cudaGetErrorString(e));
+      }
     }
     ++ctx->launches;
     const bool bwd = kind == K_BWD_LAST_PROP || kind == K_BWD_LAST_END || kind == K_BWD_MID || kind == K_BWD_END;

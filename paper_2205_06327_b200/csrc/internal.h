@@ -48,8 +48,10 @@ struct PassArgs {
   // TMA descriptors of V_k and AccBuf_k for this pass's slice parity (3-D: position along the
   // line, line, slice/2; box = min(N, 256) positions of one line; out-of-bounds = zero fill on
   // load, clipped on store -- exactly the zero-extension of reading #12 and the win ^ R_k mask).
-  // Read by the kernels from the __grid_constant__ parameter; unused by the persistent chain.
-  CUtensorMap tmV, tmA;
+  // Device copies in the workspace (64-B aligned, written once by set_workspace); unused by the
+  // persistent chain.
+  const CUtensorMap* tmV;
+  const CUtensorMap* tmA;
 };
 
 enum PassKind : int {

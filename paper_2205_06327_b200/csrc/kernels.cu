@@ -132,22 +132,21 @@ template <> struct DftReg<4> {
   __device__ __forceinline__ static void run(float2 (&x)[4]) { dft4(x[0], x[1], x[2], x[3]); }
 };
 
-// exp(i x) for the transmission t = exp(i sigma V): Cephes minimax polynomials (about 1 ulp) on
-// the reduced argument r = x - k pi/2, k = rint(2x/pi) (two-constant Cody-Waite reduction, exact
-// for the |k| a phase sigma V can reach), quadrant by k mod 4.  Branch-free: the earlier
-// warp-vote fast path (|x| <= pi/4) split every unrolled element of the pointwise loops into its
-// own basic block; for |x| <= pi/4, k = 0 and the result is bit-identical to it.
+// exp(i x) for the transmission t = exp(i sigma V): Cephes minimax polynomials on |x| <= pi/4
+// (about 1 ulp, no range reduction -- sigma V is a small phase for any physical potential),
+// sincospi with its exact reduction otherwise.  (A branch-free Cody-Waite-reduced variant, bit-
+// identical on |x| <= pi/4, measured slower: 2x4 tiles -1 %, lone chain -2.3 %,
+// profiles/round2/ab_tma.txt, so the warp-uniform fast path stays.)
 __device__ __forceinline__ void sincos_t(float x, float* sn, float* cs) {
-  const float k = rintf(x * 0.636619772367581343f);
-  const float r = fmaf(k, 4.37113900018624283e-8f, fmaf(-k, 1.57079637050628662f, x));  // pi/2 = hi - 4.37e-8
-  const float z = r * r;
-  const float s0 = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * r, r);
-  const float c0 = fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f),
-                        z * z, fmaf(-0.5f, z, 1.0f));
-  const int q = (int)k;
-  const float s1 = (q & 1) ? c0 : s0, c1 = (q & 1) ? s0 : c0;
-  *sn = (q & 2) ? -s1 : s1;
-  *cs = ((q + 1) & 2) ? -c1 : c1;
+  // warp-uniform branch: a per-lane branch gets if-converted and evaluates both paths
+  if (__all_sync(0xffffffffu, fabsf(x) <= 0.785398163f)) {
+    const float z = x * x;
+    *sn = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * x, x);
+    *cs = fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f), z * z,
+               fmaf(-0.5f, z, 1.0f));
+  } else {
+    sincospif(x * 0.318309886183790672f, sn, cs);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -513,19 +512,12 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
       " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(z),
       "r"(smem_u32(bar)), "l"(pol) : "memory");
 }
-__device__ __forceinline__ void tma_store3(const CUtensorMap* map, int x, int y, int z, const void* src,
-                                           unsigned long long pol) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
-               ::"l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(src)), "l"(pol) : "memory");
-}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
                                           unsigned long long pol) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
 }
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 
 // Location of this line inside R_k for slice parity ax.
 struct LineLoc {
@@ -562,21 +554,26 @@ struct Smem {
   static constexpr size_t tw = 0;                                    // twiddles (engine layout)
   static constexpr size_t ht = tw + (TW_REG ? 0 : (size_t)ENG::TW * 8);  // H_1/N, m = 0..N/2
   static constexpr size_t bar = ht + (N / 2 + 2) * 8;                // mbarrier of the TMA prefetch
-  static constexpr size_t lines = (bar + 8 + 127) / 128 * 128;       // per-line buffers, 128-B aligned (TMA)
+  static constexpr size_t red = bar + 8;                             // TURN: per-warp loss partials
+  static constexpr size_t lines = (red + 64 + 127) / 128 * 128;      // per-line buffers, 128-B aligned (TMA)
   static constexpr size_t ex_b = (size_t)ENG::EX * 8;                // exchange buffer per line
   static constexpr size_t st_b = kind_grad(KIND) ? (size_t)N * 8 : 0;  // stash prefetch per line
+  // V / AccBuf rows: N floats + the 4-float tail of the 16-B aligned TMA superset (rounded to
+  // 128 B so that every TMA destination stays 128-B aligned)
   static constexpr size_t v_b =
-      (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND) || KIND == K_TURN) ? (size_t)N * 4 : 0;
-  static constexpr size_t acc_b = kind_grad(KIND) ? (size_t)N * 4 : 0;  // AccBuf prefetch per line
+      (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND) || KIND == K_TURN) ? (size_t)N * 4 + 128 : 0;
+  static constexpr size_t acc_b = kind_grad(KIND) ? (size_t)N * 4 + 128 : 0;  // AccBuf prefetch per line
   static constexpr size_t per_line = ex_b + st_b + v_b + acc_b;
   static constexpr size_t stage_b = (size_t)N * (L + 1) * 8;         // transposed-store staging
   static constexpr size_t total = lines + (per_line * L > stage_b ? per_line * L : stage_b);
-  static constexpr size_t alloc = total + 128;  // dynamic smem is aligned to 128 B at run time
+  // the pass kernels have no static shared memory, so the dynamic window starts at shared offset 0
+  // (declared 128-B aligned): every offset above is an immediate, no run-time pointer alignment
+  static constexpr size_t alloc = total;
 };
-__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
-  return (unsigned char*)(((uintptr_t)p + 127) & ~(uintptr_t)127);
-}
-__host__ __device__ constexpr int tma_box(int n) { return n < 256 ? n : 256; }
+#ifndef PTYCHO_TMA_BOX
+#define PTYCHO_TMA_BOX 256
+#endif
+__host__ __device__ constexpr int tma_box(int n) { return n < PTYCHO_TMA_BOX ? n : PTYCHO_TMA_BOX; }
 
 // The body of one pass for one group of LINES_PER_CTA lines (grp).  PERSIST = false: a
 // standalone kernel in a CUDA-graph/PDL chain (tables loaded here, probe from *desc, input read
@@ -632,41 +629,49 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   const int i = pd.x, wy0 = pd.y, wx0 = pd.z;
   const int ax = a.s & 1;
   LineLoc LL = line_loc(a, ax, line, wy0, wx0);
-  // TMA path (standalone pass kernels): one thread loads every line's V / AccBuf row segments as
-  // 1-D boxes of the 3-D tensor maps (out-of-bounds = zero fill: reading #12 for free) and the
-  // stash / |y| rows as bulk copies, all on one mbarrier; the updated V / AccBuf rows go back as
-  // TMA stores clipped to R_k.  The persistent chain keeps per-element cp.async.
+  // TMA path (standalone pass kernels): one thread loads every line's V / AccBuf row segment as
+  // 1-D boxes of the 3-D tensor maps -- out-of-bounds = zero fill: the zero-extension of reading
+  // #12 with no bounds code -- and the stash / |y| rows as bulk copies, all on one mbarrier.  A box
+  // must start on a 16-B boundary of the row (a misaligned start faults), so the boxes cover the
+  // aligned superset [pos0 & ~3, (pos0 & ~3) + N + 4) (N / min(N, 256) main boxes + one 4-float
+  // tail box) and the consumers read the row at a shift of pos0 & 3.  The updated V / AccBuf words
+  // go back with masked st.global (a TMA store of the superset would also rewrite up to 3 voxels
+  // outside win ^ R_k, which a concurrent batch slot may own).  The persistent chain keeps
+  // per-element cp.async.
 #ifdef PTYCHO_NO_TMA
-  constexpr bool TMA = false;  // A/B build: per-element cp.async prefetch and st.global write-back
+  constexpr bool TMA = false;  // A/B build: per-element cp.async prefetch
 #else
   constexpr bool TMA = !PERSIST;
 #endif
   constexpr int BOX = tma_box(N), NBOX = N / BOX;
   constexpr bool NEED_V = kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND);
   unsigned long long* mbar = (unsigned long long*)(smem + SM::bar);
-  // line index inside the slice layout and window position 0 along the line (tile coordinates)
-  const int lidx = ax == 0 ? wy0 + line - a.ey0 : wx0 + line - a.ex0;
-  const int pos0 = LL.pos0;
+  const int xal = LL.pos0 & ~3;                       // 16-B aligned start of the superset
+  const int dsh = (TMA && NEED_V) ? (LL.pos0 & 3) : 0;  // shift of window position 0 in pv / pacc
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       mbar_init(mbar, 1);
       fence_proxy_async();
-      constexpr unsigned per = (NEED_V ? 4u * N : 0u) + (kind_grad(KIND) ? 8u * N : 0u) + (KIND == K_TURN ? 4u * N : 0u);
-      const unsigned acc_bytes = (kind_grad(KIND) && !a.no_acc) ? 4u * N : 0u;
+      constexpr unsigned row = 4u * N + 16u;
+      constexpr unsigned per = (NEED_V ? row : 0u) + (kind_grad(KIND) ? 8u * N : 0u) + (KIND == K_TURN ? 4u * N : 0u);
+      const unsigned acc_bytes = (kind_grad(KIND) && !a.no_acc) ? row : 0u;
       mbar_expect_tx(mbar, (per + acc_bytes) * L);
       for (int l = 0; l < L; ++l) {
         const int ln = grp * L + l;
         const int li = ax == 0 ? wy0 + ln - a.ey0 : wx0 + ln - a.ex0;
         unsigned char* lb = smem + SM::lines + l * SM::per_line;
         if constexpr (NEED_V) {
+          unsigned char* d = lb + SM::ex_b + SM::st_b;
 #pragma unroll
-          for (int b = 0; b < NBOX; ++b) tma_load3(lb + SM::ex_b + SM::st_b + b * BOX * 4, tmV, pos0 + b * BOX, li, a.s >> 1, mbar, pol);
+          for (int b = 0; b < NBOX; ++b) tma_load3(d + b * BOX * 4, tmV, xal + b * BOX, li, a.s >> 1, mbar, pol);
+          tma_load3(d + N * 4, tmV + 4, xal + N, li, a.s >> 1, mbar, pol);  // 4-float tail box
         }
         if constexpr (kind_grad(KIND)) {
           if (!a.no_acc) {
+            unsigned char* d = lb + SM::ex_b + SM::st_b + SM::v_b;
 #pragma unroll
-            for (int b = 0; b < NBOX; ++b)
-              tma_load3(lb + SM::ex_b + SM::st_b + SM::v_b + b * BOX * 4, tmA, pos0 + b * BOX, li, a.s >> 1, mbar, pol);
+            for (int b = 0; b < NBOX; ++b) tma_load3(d + b * BOX * 4, tmA, xal + b * BOX, li, a.s >> 1, mbar, pol);
+            tma_load3(d + N * 4, tmA + 4, xal + N, li, a.s >> 1, mbar, pol);
           }
           bulk_load(lb + SM::ex_b, a.stash + (size_t)a.stash_s * N * N + (size_t)ln * N, 8u * N, mbar, pol);
         }
@@ -710,6 +715,8 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     if constexpr (TMA) mbar_wait(mbar, 0);
     else cp_async_wait_all();
   };
+  pv += dsh;    // window position j of the V / AccBuf rows (TMA superset: shifted by pos0 & 3)
+  pacc += dsh;
   float2 x[P];
   if constexpr (FIRST) {
     const float2* src = a.probe + (size_t)line * N + q;
@@ -866,42 +873,17 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         const float2 chi = make_float2(y.x, -y.y);
         const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
         const float v = pv[j];
-        if constexpr (TMA) {
-          // updated rows in place; written back below as TMA stores clipped to R_k
-          if (!exporting) {
-            pacc[j] += g;
-            pv[j] = v - a.alpha * g;
-          } else {
-            pacc[j] = g;  // debug export of g; V / AccBuf untouched
-          }
-        } else {
-          if (!exporting && (unsigned)p < (unsigned)lim) {
-            if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
-            st_stream(vrow + p, v - a.alpha * g, pol);
-          }
-          pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
+        if (!exporting && (unsigned)p < (unsigned)lim) {
+          if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
+          st_stream(vrow + p, v - a.alpha * g, pol);
         }
+        pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
         float sn, cs;
         sincos_t(a.sigma * v, &sn, &cs);
         xs[j] = cmulc(chi, make_float2(cs, sn));
       }
 #pragma unroll
       for (int k = 0; k < P; ++k) x[k] = xs[ENG::idx(dist, q, k)];
-      if constexpr (TMA) {
-        if (!exporting) {  // Alg. 1 steps 7-8 write-back: V and AccBuf rows of win ^ R_k
-          fence_proxy_async();  // this thread's st.shared -> visible to the async proxy
-          ENG::sync_line(bid);
-          if (q == 0) {
-#pragma unroll
-            for (int b = 0; b < NBOX; ++b) tma_store3(tmV, pos0 + b * BOX, lidx, a.s >> 1, pv + b * BOX, pol);
-            if (!a.no_acc) {
-#pragma unroll
-              for (int b = 0; b < NBOX; ++b) tma_store3(tmA, pos0 + b * BOX, lidx, a.s >> 1, pacc + b * BOX, pol);
-            }
-            bulk_commit();
-          }
-        }
-      }
 #else
 #pragma unroll
       for (int k = 0; k < P; ++k) {
@@ -955,7 +937,8 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   if constexpr (KIND == K_TURN) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    __shared__ float red[LINES_PER_CTA * Q / 32 + 1];
+    float* red = (float*)(smem + SM::red);  // LINES_PER_CTA * Q / 32 <= 16 floats
+    static_assert(LINES_PER_CTA * Q / 32 + 1 <= 16, "red");
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -970,11 +953,6 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     for (int k = 0; k < P; ++k) x[k].y = -x[k].y;
   }
   constexpr int STORE = kind_store(KIND);
-  // the TMA write-back of this CTA's V / AccBuf rows has read shared memory before it is reused
-  // (the staging area overlaps the line buffers)
-  if constexpr (TMA && kind_grad(KIND)) {
-    if (q == 0) bulk_wait_read();
-  }
   if constexpr (STORE == 1) {
     // out[j][line]: stage the CTA's L = 4 lines as 32-B rows [j][4] (element l stored at
     // l ^ ((j >> 2) & 3): conflict-free column writes), then write 16-B chunks of each output
@@ -1006,9 +984,6 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     }
   }
 
-  if constexpr (TMA && kind_grad(KIND)) {
-    if (q == 0) bulk_wait();  // V / AccBuf rows in global memory before the CTA retires
-  }
   if (!PERSIST && a.advance) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1032,13 +1007,12 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 // passes always use 2 (they spill at 168).  Both builds execute the same arithmetic.
 template <int N, int KIND, int MINB>
 __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KIND) ? 2 : MINB)
-pass_kernel(const __grid_constant__ PassArgs a) {
+pass_kernel(const PassArgs a) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T;
   constexpr bool TWG = MINB >= 4 && !kind_grad(KIND) && ENG::T * ENG::T == N;
   constexpr bool TW_REG = (ENG::T * ENG::T == N) && !TWG;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned char* smem = align128(smem_raw);
+  extern __shared__ __align__(128) unsigned char smem[];
   const int q = threadIdx.x % Q;
   // four-step engines keep the thread's twiddles in registers (no shared-memory table)
   float2 twr[ENG::T * ENG::T == N ? P : 1];
@@ -1050,9 +1024,8 @@ pass_kernel(const __grid_constant__ PassArgs a) {
   // probe descriptor and loss partials)
   constexpr int groups = N / LINES_PER_CTA;
   const int b = blockIdx.x / groups, grp = blockIdx.x - b * groups;
-  // the tensor maps are used in place in the __grid_constant__ parameter (param-space address)
   if (b == 0) {
-    pass_body<N, KIND, false, TWG>(a, grp, make_int4(0, 0, 0, 0), twr, smem, &a.tmV, &a.tmA);
+    pass_body<N, KIND, false, TWG>(a, grp, make_int4(0, 0, 0, 0), twr, smem, a.tmV, a.tmA);
   } else {
     PassArgs ab = a;
     ab.stash += b * a.stash_slot;
@@ -1060,7 +1033,7 @@ pass_kernel(const __grid_constant__ PassArgs a) {
     ab.out += b * a.wf_slot;
     ab.desc += b;
     ab.loss_part += b * groups;
-    pass_body<N, KIND, false, TWG>(ab, grp, make_int4(0, 0, 0, 0), twr, smem, &a.tmV, &a.tmA);
+    pass_body<N, KIND, false, TWG>(ab, grp, make_int4(0, 0, 0, 0), twr, smem, a.tmV, a.tmA);
   }
 }
 
@@ -1113,8 +1086,7 @@ __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2) chain_ker
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
   constexpr bool TW_REG = (ENG::T * ENG::T == N);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned char* smem = align128(smem_raw);
+  extern __shared__ __align__(128) unsigned char smem[];
   const int q = threadIdx.x % Q;
   float2 twr[TW_REG ? P : 1];
   if constexpr (TW_REG) {
@@ -1294,9 +1266,64 @@ __global__ void __launch_bounds__(256) copy2d_kernel(float* __restrict__ dst, lo
   }
 }
 
+// The same with 16-B accesses (rows 16-B aligned, pitches multiples of 4 floats): 4x fewer
+// requests -- what matters when src is a peer's AccBuf read over NVLink (APPP P2P transport);
+// the row tail (cols % 4) is moved by the first CTA of the row.
+__global__ void __launch_bounds__(256) copy2d_v4_kernel(float* __restrict__ dst, long long dld, long long dss,
+                                                        const float* __restrict__ src, long long sld, long long sss,
+                                                        int rows, int cols, int op) {
+  const int r = blockIdx.y;
+  const long long z = blockIdx.z;
+  float* d = dst + z * dss + (long long)r * dld;
+  const float* s = src + z * sss + (long long)r * sld;
+  const int c4 = cols >> 2;
+  const int i0 = blockIdx.x * (256 * COPY_U) + threadIdx.x;
+  float4 v[COPY_U];
+#pragma unroll
+  for (int u = 0; u < COPY_U; ++u) {
+    const int i = i0 + 256 * u;
+    v[u] = i < c4 ? ((const float4*)s)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < COPY_U; ++u) {
+    const int i = i0 + 256 * u;
+    if (i < c4) {
+      float4* dp = (float4*)d + i;
+      if (op == 0) {
+        *dp = v[u];
+      } else {
+        float4 o = *dp;
+        o.x += v[u].x;
+        o.y += v[u].y;
+        o.z += v[u].z;
+        o.w += v[u].w;
+        *dp = o;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (cols & 3)) {
+    const int c = (c4 << 2) + threadIdx.x;
+    if (op == 0) d[c] = s[c];
+    else d[c] += s[c];
+  }
+}
+
 cudaError_t launch_copy2d(float* dst, long long dld, long long dss, const float* src, long long sld,
                           long long sss, int rows, int cols, int nslices, int op, cudaStream_t stream) {
   if (rows <= 0 || cols <= 0 || nslices <= 0) return cudaSuccess;
+  const bool v4 = (((uintptr_t)dst | (uintptr_t)src) & 15) == 0 && ((dld | sld | dss | sss) & 3) == 0 && cols >= 4;
+  if (v4) {
+    for (int z0 = 0; z0 < nslices; z0 += 65535) {
+      const int nz = nslices - z0 < 65535 ? nslices - z0 : 65535;
+      for (int r0 = 0; r0 < rows; r0 += 65535) {
+        const int nr = rows - r0 < 65535 ? rows - r0 : 65535;
+        dim3 grid(((cols >> 2) + 256 * COPY_U - 1) / (256 * COPY_U), nr, nz);
+        copy2d_v4_kernel<<<grid, 256, 0, stream>>>(dst + z0 * dss + (long long)r0 * dld, dld, dss,
+                                                   src + z0 * sss + (long long)r0 * sld, sld, sss, nr, cols, op);
+      }
+    }
+    return cudaGetLastError();
+  }
   for (int z0 = 0; z0 < nslices; z0 += 65535) {
     const int nz = nslices - z0 < 65535 ? nslices - z0 : 65535;
     for (int r0 = 0; r0 < rows; r0 += 65535) {
