@@ -280,6 +280,13 @@ ptycho_status ptycho_profile_chain(ptycho_ctx ctx, int32_t tile, int64_t first, 
  * Synchronizes. */
 ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out);
 
+/* Ordering checks (compute-sanitizer is not available on this pool): a library
+ * built with -DPTYCHO_DEBUG_CHECKS (lib/libptycho_debug.so) re-reads, after griddepcontrol.wait,
+ * every V / AccBuf / stash word a pass prefetched BEFORE the grid dependency resolved and ORs a bit
+ * into an error word on any mismatch: 1 V (gradient pass), 2 AccBuf, 4 stash, 8 V (forward pass).
+ * Synchronizes, returns and clears the bits; *checks_built = 0 for the product library (bits 0). */
+ptycho_status ptycho_debug_errors(ptycho_ctx ctx, uint32_t* bits, int32_t* checks_built);
+
 /* ---------------------------------------------------------------------------------------------
  * Debug exports (same library; used by the parity tests).  All synchronize; host buffers.
  * ------------------------------------------------------------------------------------------- */

@@ -10,6 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libptycho.so")
+DEBUG_LIB = os.path.join(LIBDIR, "libptycho_debug.so")
 SOURCES = ["kernels.cu", "api.cu"]
 HEADERS = ["internal.h", "twiddle32.h"]
 
@@ -31,6 +32,8 @@ def _stale() -> bool:
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "ptycho.h")]
     if not os.path.exists(DEMO) or os.path.getmtime(DEMO_SRC) > os.path.getmtime(DEMO):
+        return True
+    if not os.path.exists(DEBUG_LIB) or os.path.getmtime(DEBUG_LIB) < t:
         return True
     return any(os.path.getmtime(d) > t for d in deps)
 
@@ -66,6 +69,8 @@ def build(force: bool = False, verbose: bool = True, defines=(), out=None) -> st
     subprocess.check_call(link)
     if out is None:
         build_demo(verbose)
+        # ordering-check variant (ptycho_debug_errors; tests/test_gpu_ordering.py)
+        build(force=True, verbose=verbose, defines=list(defines) + ["PTYCHO_DEBUG_CHECKS"], out=DEBUG_LIB)
     return lib_out
 
 

@@ -672,6 +672,7 @@ extern "C" ptycho_status ptycho_set_workspace(ptycho_ctx ctx, void* workspace_de
     CK(cudaMemsetAsync(t.loss_part, 0, ctx->batch * (n / LINES_PER_CTA) * sizeof(double), ctx->stream));
     CK(cudaMemsetAsync(t.amp, 0, std::max<size_t>(t.probes.size(), 1) * n * n * sizeof(float), ctx->stream));
   }
+  CK(cudaMemsetAsync(ctx->iscratch, 0, 64 * sizeof(int), ctx->stream));
   PASS(zero_tiles(ctx, true, true));
   if (ctx->flags) CK(cudaMemsetAsync(ctx->flags, 0, 2 * std::max<size_t>(ctx->hops.size(), 1) * sizeof(unsigned),
                                      ctx->stream));
@@ -977,6 +978,7 @@ static PassArgs base_args(ptycho_ctx ctx, const Tile& t) {
   a.stash_store = 1;
   a.wf_slot = (long long)ctx->cfg.n * ctx->cfg.n;
   a.no_acc = ctx->hve ? 1 : 0;
+  a.dbg = (unsigned*)(ctx->iscratch + 32);  // error bits of PTYCHO_DEBUG_CHECKS builds
   return a;
 }
 
@@ -1778,6 +1780,20 @@ extern "C" ptycho_status ptycho_synchronize(ptycho_ctx ctx) {
     if (ctx->tiles[k].stream) CK(cudaStreamSynchronize(ctx->tiles[k].stream));
   if (ctx->copy_stream) CK(cudaStreamSynchronize(ctx->copy_stream));
   return check_p2p(ctx);
+}
+
+extern "C" ptycho_status ptycho_debug_errors(ptycho_ctx ctx, uint32_t* bits, int32_t* checks_built) {
+  PASS(need_ws(ctx));
+  if (!bits || !checks_built) return fail(ctx, PTYCHO_EARG, "outputs are NULL");
+#ifdef PTYCHO_DEBUG_CHECKS
+  *checks_built = 1;
+#else
+  *checks_built = 0;
+#endif
+  PASS(ptycho_synchronize(ctx));
+  CK(cudaMemcpy(bits, ctx->iscratch + 32, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(ctx->iscratch + 32, 0, sizeof(uint32_t)));
+  return PTYCHO_OK;
 }
 
 extern "C" ptycho_status ptycho_kernel_launches(ptycho_ctx ctx, int64_t* count) {

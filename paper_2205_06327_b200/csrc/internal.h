@@ -52,6 +52,7 @@ struct PassArgs {
   // persistent chain.
   const CUtensorMap* tmV;
   const CUtensorMap* tmA;
+  unsigned* dbg;            // PTYCHO_DEBUG_CHECKS builds: ordering / staleness error bits (else unused)
 };
 
 enum PassKind : int {

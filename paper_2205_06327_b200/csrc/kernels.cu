@@ -134,12 +134,14 @@ template <> struct DftReg<4> {
 
 // exp(i x) for the transmission t = exp(i sigma V): Cephes minimax polynomials on |x| <= pi/4
 // (about 1 ulp, no range reduction -- sigma V is a small phase for any physical potential),
-// sincospi with its exact reduction otherwise.  (A branch-free Cody-Waite-reduced variant, bit-
-// identical on |x| <= pi/4, measured slower: 2x4 tiles -1 %, lone chain -2.3 %,
-// profiles/round2/ab_tma.txt, so the warp-uniform fast path stays.)
+// sincospi with its exact reduction otherwise.  The choice is made ONCE per pointwise step for the
+// whole warp (small_phases: one vote over every element the warp's threads hold), so the unrolled
+// step loops are branch-free and their elements interleave (a per-element vote split every
+// element into its own basic block).  A branch-free Cody-Waite-reduced variant measured slower
+// (2x4 tiles -1 %, lone chain -2.3 %, profiles/round2/ab_tma.txt).
+template <bool FAST>
 __device__ __forceinline__ void sincos_t(float x, float* sn, float* cs) {
-  // warp-uniform branch: a per-lane branch gets if-converted and evaluates both paths
-  if (__all_sync(0xffffffffu, fabsf(x) <= 0.785398163f)) {
+  if (FAST) {
     const float z = x * x;
     *sn = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * x, x);
     *cs = fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f), z * z,
@@ -148,6 +150,16 @@ __device__ __forceinline__ void sincos_t(float x, float* sn, float* cs) {
     sincospif(x * 0.318309886183790672f, sn, cs);
   }
 }
+// |sigma v| <= pi/4 for every v[idx(k)], k < P, of every thread of the warp (rounding of sigma*v is
+// monotone in |v|, so the max decides exactly what the per-element test did)
+template <int P, typename Idx>
+__device__ __forceinline__ bool small_phases(const float* v, float sigma, Idx idx) {
+  float m = 0.f;
+#pragma unroll
+  for (int k = 0; k < P; ++k) m = fmaxf(m, fabsf(v[idx(k)]));
+  return __all_sync(0xffffffffu, fabsf(sigma * m) <= 0.785398163f);
+}
+template <bool B> struct Bool { static constexpr bool value = B; };
 
 // ------------------------------------------------------------------------------------------
 // FFT engines.  A line of N complex values is held by T threads, E = N/T elements each.
@@ -774,17 +786,30 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       float2* xs = ex + q;  // rolled through the idle exchange buffer (instruction-cache footprint)
 #pragma unroll
       for (int k = 0; k < P; ++k) xs[Q * k] = x[k];
-#pragma unroll kStepUnroll
-      for (int k = 0; k < P; ++k) {
-        const float v = pv[q + Q * k];
-        float sn, cs;
-        sincos_t(a.sigma * v, &sn, &cs);
-        float2 y = xs[Q * k];
-        if (PL.transmit_cp) y.y = -y.y;
-        const float2 phi = cmul(y, make_float2(cs, sn));
-        xs[Q * k] = phi;
-        if (keep) st_stream(stp + Q * k, phi, pol);
+#ifdef PTYCHO_DEBUG_CHECKS
+      {  // the V row prefetched before griddepcontrol.wait (TMA) equals V in L2 now: no stale read
+        const float* vr = a.V + (long long)a.s * a.slice_stride + LL.row;
+        for (int k = 0; k < P; ++k) {
+          const int p = LL.pos0 + q + Q * k;
+          if (LL.ok && (unsigned)p < (unsigned)LL.plim && __ldcg(vr + p) != pv[q + Q * k]) atomicOr(a.dbg, 8u);
+        }
       }
+#endif
+      auto body = [&](auto fast) {
+#pragma unroll kStepUnroll
+        for (int k = 0; k < P; ++k) {
+          const float v = pv[q + Q * k];
+          float sn, cs;
+          sincos_t<decltype(fast)::value>(a.sigma * v, &sn, &cs);
+          float2 y = xs[Q * k];
+          if (PL.transmit_cp) y.y = -y.y;
+          const float2 phi = cmul(y, make_float2(cs, sn));
+          xs[Q * k] = phi;
+          if (keep) st_stream(stp + Q * k, phi, pol);
+        }
+      };
+      if (small_phases<P>(pv, a.sigma, [&](int k) { return q + Q * k; })) body(Bool<true>());
+      else body(Bool<false>());
 #pragma unroll
       for (int k = 0; k < P; ++k) x[k] = xs[Q * k];
 #else
@@ -792,7 +817,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       for (int k = 0; k < P; ++k) {
         const float v = pv[q + Q * k];
         float sn, cs;
-        sincos_t(a.sigma * v, &sn, &cs);
+        sincos_t<false>(a.sigma * v, &sn, &cs);
         float2 y = x[k];
         if (PL.transmit_cp) y.y = -y.y;
         x[k] = cmul(y, make_float2(cs, sn));
@@ -831,18 +856,22 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       float2* xs = ex;
 #pragma unroll
       for (int k = 0; k < P; ++k) xs[ENG::idx(dist, q, k)] = x[k];
+      auto body = [&](auto fast) {
 #pragma unroll kStepUnroll
-      for (int k = 0; k < P; ++k) {
-        const int j = ENG::idx(dist, q, k);
-        float2 phi = xs[j];
-        if (pending) {
-          phi.y = -phi.y;
-          st_stream(stp + j, phi, pol);
+        for (int k = 0; k < P; ++k) {
+          const int j = ENG::idx(dist, q, k);
+          float2 phi = xs[j];
+          if (pending) {
+            phi.y = -phi.y;
+            st_stream(stp + j, phi, pol);
+          }
+          float sn, cs;
+          sincos_t<decltype(fast)::value>(a.sigma * pv[j], &sn, &cs);
+          xs[j] = cmulc(phi, make_float2(cs, sn));
         }
-        float sn, cs;
-        sincos_t(a.sigma * pv[j], &sn, &cs);
-        xs[j] = cmulc(phi, make_float2(cs, sn));
-      }
+      };
+      if (small_phases<P>(pv, a.sigma, [&](int k) { return ENG::idx(dist, q, k); })) body(Bool<true>());
+      else body(Bool<false>());
 #pragma unroll
       for (int k = 0; k < P; ++k) x[k] = xs[ENG::idx(dist, q, k)];
     } else if (has_step(PL, S_GRAD) && st == S_GRAD) {
@@ -864,24 +893,43 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       float2* xs = ex;
 #pragma unroll
       for (int k = 0; k < P; ++k) xs[ENG::idx(dist, q, k)] = x[k];
-#pragma unroll kStepUnroll
-      for (int k = 0; k < P; ++k) {
-        const int j = ENG::idx(dist, q, k);
-        const int p = LL.pos0 + j;
-        const float2 ph = pst[j];
-        const float2 y = xs[j];
-        const float2 chi = make_float2(y.x, -y.y);
-        const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
-        const float v = pv[j];
-        if (!exporting && (unsigned)p < (unsigned)lim) {
-          if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
-          st_stream(vrow + p, v - a.alpha * g, pol);
+#ifdef PTYCHO_DEBUG_CHECKS
+      {  // V / AccBuf / stash rows prefetched before griddepcontrol.wait equal their L2 values now
+        const float2* sr = a.stash + (size_t)a.stash_s * N * N + (size_t)line * N;
+        for (int k = 0; k < P; ++k) {
+          const int j = ENG::idx(dist, q, k);
+          const int p = LL.pos0 + j;
+          if ((unsigned)p < (unsigned)lim) {
+            if (__ldcg(vrow + p) != pv[j]) atomicOr(a.dbg, 1u);
+            if (!a.no_acc && __ldcg(arow + p) != pacc[j]) atomicOr(a.dbg, 2u);
+          }
+          const float2 sg = __ldcg(sr + j);
+          if (sg.x != pst[j].x || sg.y != pst[j].y) atomicOr(a.dbg, 4u);
         }
-        pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
-        float sn, cs;
-        sincos_t(a.sigma * v, &sn, &cs);
-        xs[j] = cmulc(chi, make_float2(cs, sn));
       }
+#endif
+      auto body = [&](auto fast) {
+#pragma unroll kStepUnroll
+        for (int k = 0; k < P; ++k) {
+          const int j = ENG::idx(dist, q, k);
+          const int p = LL.pos0 + j;
+          const float2 ph = pst[j];
+          const float2 y = xs[j];
+          const float2 chi = make_float2(y.x, -y.y);
+          const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
+          const float v = pv[j];
+          if (!exporting && (unsigned)p < (unsigned)lim) {
+            if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
+            st_stream(vrow + p, v - a.alpha * g, pol);
+          }
+          pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
+          float sn, cs;
+          sincos_t<decltype(fast)::value>(a.sigma * v, &sn, &cs);
+          xs[j] = cmulc(chi, make_float2(cs, sn));
+        }
+      };
+      if (small_phases<P>(pv, a.sigma, [&](int k) { return ENG::idx(dist, q, k); })) body(Bool<true>());
+      else body(Bool<false>());
 #pragma unroll
       for (int k = 0; k < P; ++k) x[k] = xs[ENG::idx(dist, q, k)];
 #else
@@ -900,7 +948,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         }
         pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
         float sn, cs;
-        sincos_t(a.sigma * v, &sn, &cs);
+        sincos_t<false>(a.sigma * v, &sn, &cs);
         x[k] = cmulc(chi, make_float2(cs, sn));
       }
 #endif

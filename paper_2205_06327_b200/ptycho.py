@@ -72,6 +72,7 @@ _SIGS = {
     "ptycho_kernel_launches": [_P, _c.POINTER(_c.c_int64)],
     "ptycho_profile_chain": [_P, _c.c_int32, _c.c_int64, _c.c_int64, _P, _P],
     "ptycho_profile_iteration": [_P, _P],
+    "ptycho_debug_errors": [_P, _P, _P],
     "ptycho_debug_read_tile": [_P, _c.c_int32, _c.c_int32, _P],
     "ptycho_debug_write_tile": [_P, _c.c_int32, _c.c_int32, _P],
     "ptycho_debug_probe_grad": [_P, _c.c_int32, _c.c_int64, _P, _c.POINTER(_c.c_double)],
@@ -348,6 +349,13 @@ class Ptycho:
         ms = np.zeros(5, np.float64)
         self._ck(lib.ptycho_profile_iteration(self.h, ms.ctypes.data))
         return dict(zip(["total_ms", "compute_ms", "wait_ms", "comm_ms", "acc_step_ms"], (float(v) for v in ms)))
+
+    def debug_errors(self):
+        """(error bits, checks_built) of the PTYCHO_DEBUG_CHECKS ordering checks (clears the bits)."""
+        bits = ctypes.c_uint32()
+        built = ctypes.c_int32()
+        self._ck(lib.ptycho_debug_errors(self.h, ctypes.byref(bits), ctypes.byref(built)))
+        return bits.value, bool(built.value)
 
     # ---- debug exports
     def debug_read_tile(self, tile, which):

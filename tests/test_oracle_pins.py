@@ -570,22 +570,20 @@ def test_hve_spec_example_centre_tile_holds_all_nine():
     # SPEC S:480 / P:360-362 (Fig. halo_voxel_exch1 d-e): 3x3 mesh, 3x3 scan, one extra row of
     # probe locations -> the corner tile holds 4 probes, an edge tile 6, the centre tile all 9
     centers = synth.scan_centers(96, 96, 3, 3)          # centres 16, 48, 80: step 32
-    tiles = O.hve_decompose(96, 96, 3, 3, centers, 16, margin=32)
+    tiles = O.hve_decompose(96, 96, 3, 3, centers, margin=32, halo=24)
     counts = [len(t["probes"]) for t in tiles]
     assert counts == [4, 6, 4, 6, 9, 6, 4, 6, 4]
     assert tiles[4]["probes"] == list(range(9))
-    # augmented rect = bbox of the interior and the assigned 16 x 16 windows
-    assert tiles[4]["ext"] == (8, 8, 88, 88)
-    assert tiles[0]["ext"] == (0, 0, 56, 56)
+    assert tiles[4]["ext"] == (8, 8, 88, 88) and tiles[0]["ext"] == (0, 0, 56, 56)
 
 
 def test_hve_trivial_mesh_and_too_small_tiles():
     centers = synth.scan_centers(96, 96, 6, 6)
-    t = O.hve_decompose(96, 96, 1, 1, centers, 16, margin=16)
+    t = O.hve_decompose(96, 96, 1, 1, centers, margin=16, halo=8)
     assert len(t) == 1 and t[0]["probes"] == list(range(36)) and t[0]["ext"] == (0, 0, 96, 96)
     with pytest.raises(O.TileTooSmall):
-        O.hve_decompose(96, 96, 6, 6, centers, 16, margin=32)  # interiors 16 < halo reach
-    O.hve_decompose(96, 96, 3, 3, centers, 16, margin=16)      # interiors 32: fine
+        O.hve_decompose(96, 96, 6, 6, centers, margin=16, halo=24)  # interiors 16 < halo 24
+    O.hve_decompose(96, 96, 6, 6, centers, margin=16, halo=16)      # halo = interior: fine
 
 
 def _hve_problem(seed=41):
@@ -603,7 +601,7 @@ def test_hve_one_tile_is_plain_sgd():
     # 1x1: HVE is sequential per-probe SGD, i.e. Alg. 1 on one tile without the accumulated step
     p, vt, centers, cfg, amps = _hve_problem()
     v0 = 0.5 * vt
-    a, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 1, 1, 8, 2, alpha=2.0)
+    a, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 1, 1, 8, 8, 2, alpha=2.0)
     b, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 2, alpha=2.0, alpha_acc=0.0)
     assert np.array_equal(a, b)
 
@@ -613,10 +611,10 @@ def test_hve_all_probes_everywhere_equals_single_tile():
     # full reconstruction on the whole object -> the exchange is a no-op and the stitch equals 1x1
     p, vt, centers, cfg, amps = _hve_problem()
     v0 = 0.5 * vt
-    tiles = O.hve_decompose(48, 48, 2, 2, centers, 16, margin=100)
+    tiles = O.hve_decompose(48, 48, 2, 2, centers, margin=100, halo=24)
     assert all(len(t["probes"]) == 36 and t["ext"] == (0, 0, 48, 48) for t in tiles)
-    a, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 2, 2, 100, 2, alpha=2.0)
-    b, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 2, alpha=2.0)
+    a, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 2, 2, 100, 24, 2, alpha=2.0)
+    b, _, _ = O.hve_reconstruct(v0, p, amps, centers, cfg, 1, 1, 0, 0, 2, alpha=2.0)
     assert np.array_equal(a, b)
 
 
@@ -624,13 +622,13 @@ def test_hve_halos_equal_owner_interiors_after_exchange():
     # after each copy-paste every halo voxel equals its owner's interior voxel bitwise
     p, vt, centers, cfg, amps = _hve_problem()
     v0 = 0.5 * vt
-    out, _, vks = O.hve_reconstruct(v0, p, amps, centers, cfg, 2, 2, 8, 1, alpha=2.0)
-    tiles = O.hve_decompose(48, 48, 2, 2, centers, 16, margin=8)
+    out, _, vks = O.hve_reconstruct(v0, p, amps, centers, cfg, 2, 2, 8, 12, 1, alpha=2.0)
+    tiles = O.hve_decompose(48, 48, 2, 2, centers, margin=8, halo=12)
     for vk, t in zip(vks, tiles):
         y0, x0, y1, x1 = t["ext"]
         assert np.array_equal(vk, out[:, y0:y1, x0:x1])  # every voxel of R_k = the stitched (owner) value
     # and the result differs from GD's (the methods are not equivalent with partial probe sets)
-    gd, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 2, 2, 8, 1, alpha=2.0, alpha_acc=0.0)
+    gd, _, _, _ = O.reconstruct(v0, p, amps, centers, cfg, 2, 2, 12, 1, alpha=2.0, alpha_acc=0.0)
     assert not np.array_equal(out, gd)
 
 

@@ -1,0 +1,2 @@
+timeout 600 python tools/sanitize_tiny.py > gpurun_out/san_plain_racecheck.log 2>&1 && \
+timeout 1500 compute-sanitizer --tool racecheck  --print-limit 50 python tools/sanitize_tiny.py > gpurun_out/san_racecheck.log 2>&1; echo rc=$?; tail -5 gpurun_out/san_racecheck.log
