@@ -122,6 +122,7 @@ struct ptycho_ctx_s {
   bool debug_sync = false;  // PTYCHO_DEBUG_SYNC: synchronize after every direct pass launch
   int slab = 0;  // slices per APPP slab in ptycho_iterate (0 = passes after the whole segment)
   bool persist = false;  // run probe chains in the persistent cooperative chain kernel
+  bool cluster = false;  // N <= 256: cluster-resident probe chains (wavefield in DSMEM)
   bool hve = false;      // Halo Voxel Exchange baseline (ptycho_set_tiles_hve)
   int hve_margin = 0;    // HVE probe-assignment margin (pixels)
   bool batched = false;  // opt-in batched schedule (non-overlapping windows side by side)
@@ -208,6 +209,15 @@ extern "C" ptycho_status ptycho_create(const ptycho_config* cfg, int device, voi
   if (const char* e = getenv("PTYCHO_SLAB")) ctx->slab = std::max(0, atoi(e));
   if (const char* e = getenv("PTYCHO_PERSIST")) ctx->persist = atoi(e) != 0;
   if (cfg->flags & PTYCHO_F_STASH_FREE) ctx->persist = false;  // the chain kernel keeps a full stash
+  // Opt-in (PTYCHO_CLUSTER=1), N <= 256: one 16-CTA cluster per tile runs a whole segment's probe
+  // chains with the wavefield in DSMEM.  Bit-identical to the graph + PDL chain but measured 2x
+  // slower (small 3152 vs 6307 probe-loc/s): a cluster holds at most 16 CTAs, so each SM carries 4x
+  // the lines of a standalone pass (profiles/round2/cluster_chain.txt).  Not with the stash-free
+  // ring or the persistent kernel.
+  ctx->cluster = false;
+  if (const char* e = getenv("PTYCHO_CLUSTER"))
+    ctx->cluster = atoi(e) != 0 && (cfg->n == 64 || cfg->n == 256) && !(cfg->flags & PTYCHO_F_STASH_FREE) &&
+                   !ctx->persist;
   if (const char* e = getenv("PTYCHO_P2P_TIMEOUT_S")) ctx->p2p_timeout_ns = (unsigned long long)(atof(e) * 1e9);
   if (const char* e = getenv("PTYCHO_APPP_TRANSPORT")) {
     if (!strcmp(e, "nccl")) ctx->transport_req = PTYCHO_APPP_NCCL;
@@ -1215,8 +1225,36 @@ static ptycho_status run_chain_kernel(ptycho_ctx ctx, int64_t first, const std::
   return PTYCHO_OK;
 }
 
+// Probes [first, first + cnt[k]) of every local tile k in cluster-resident chains (one 16-CTA
+// cluster per tile, up to MAX_CHAIN_TILES tiles per launch) on ctx->stream.
+static ptycho_status run_cluster_chain(ptycho_ctx ctx, int64_t first, int64_t count) {
+  PASS(amp_settle(ctx, ctx->stream));
+  ChainArgs c{};
+  int nt = 0;
+  auto flush = [&]() -> ptycho_status {
+    if (nt == 0) return PTYCHO_OK;
+    c.ntiles = nt;
+    c.first = (int)first;
+    c.S = ctx->cfg.slices;
+    CK(launch_cluster(ctx->cfg.n, c, ctx->stream));
+    ctx->launches += 1;
+    nt = 0;
+    return PTYCHO_OK;
+  };
+  for (int k : ctx->local) {
+    Tile& t = ctx->tiles[k];
+    const int64_t m = std::max<int64_t>(0, std::min<int64_t>(first + count, (int64_t)t.probes.size()) - first);
+    if (m == 0) continue;
+    c.t[nt] = base_args(ctx, t);
+    c.count[nt] = (int)m;
+    if (++nt == MAX_CHAIN_TILES) PASS(flush());
+  }
+  return flush();
+}
+
 static ptycho_status run_probes(ptycho_ctx ctx, int64_t first, int64_t count, ChainMode mode) {
   if (mode == CHAIN_GRAD && ctx->batched) return run_batched(ctx, first, count);
+  if (mode == CHAIN_GRAD && ctx->cluster) return run_cluster_chain(ctx, first, count);
   if (mode == CHAIN_GRAD && ctx->persist) {
     std::vector<int64_t> cnt(ctx->tiles.size(), 0);
     for (int k : ctx->local)
@@ -1549,7 +1587,7 @@ extern "C" ptycho_status ptycho_step(ptycho_ctx ctx) {
 // the passes and the accumulated step of a slab start as soon as every local tile reached it,
 // overlapping the backward passes of the lower slices.
 static ptycho_status segment_pipelined(ptycho_ctx ctx, int64_t first, int64_t count) {
-  if (ctx->batched) {  // batches end with whole batches: passes after the segment
+  if (ctx->batched || ctx->cluster) {  // whole batches / one cluster launch: passes after the segment
     PASS(run_probes(ctx, first, count, CHAIN_GRAD));
     PASS(appp_range(ctx, 0, ctx->cfg.slices));
     return step_range(ctx, 0, ctx->cfg.slices);

@@ -86,6 +86,9 @@ struct ChainArgs {
   unsigned* bar;                       // grid-barrier counter (zeroed before the launch)
 };
 cudaError_t launch_chain(int n, const ChainArgs& c, cudaStream_t stream);
+// Cluster-resident chain (N = 64, 256): one 16-CTA cluster per tile, the wavefield in DSMEM,
+// probes [first, first + count[t]) of tile t; in / out / bar of ChainArgs unused.
+cudaError_t launch_cluster(int n, const ChainArgs& c, cudaStream_t stream);
 
 // Launch one pass kernel (with programmatic dependent launch on `stream`).
 cudaError_t launch_pass(int n, PassKind kind, const PassArgs& a, cudaStream_t stream, bool pdl);

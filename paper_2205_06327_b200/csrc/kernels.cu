@@ -369,10 +369,11 @@ void fill_twiddles(int n, float2* tw) {
 //   adjoint      P^H = F^-1 conj(H)/N F  ->  F ; y <- (H/N) conj(y)      ; F ; result = conj(z)
 // so after the second F of a propagation the register value is the conjugate of the true field
 // ("conj pending"); the next step folds that conjugation in.
-// Unroll factor of the rolled pointwise steps (TRANSMIT / GRAD / RECON), see S_GRAD: 4 measured
-// +0.5 % over 2 (8 tiles and lone chain), 8 -1 % / -2 % (profiles/round1.md).
+// Unroll factor of the rolled pointwise steps (TRANSMIT / GRAD / RECON), see S_GRAD: round 1 (per-
+// element sincos votes) 4 > 8; with one vote per step the loops are branch-free and 8 measured
+// +0.6 % (8 tiles) / +0.5 % (lone chain) over 4 (profiles/round2/ab_unroll.txt).
 #ifndef PTYCHO_STEP_UNROLL
-#define PTYCHO_STEP_UNROLL 4
+#define PTYCHO_STEP_UNROLL 8
 #endif
 constexpr int kStepUnroll = PTYCHO_STEP_UNROLL;
 #ifndef PTYCHO_PREF_UNROLL
@@ -531,6 +532,26 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
 }
 
 
+// ---- thread-block clusters (cluster_chain_kernel)
+__device__ __forceinline__ void st_cluster_v4(const void* local_smem, unsigned rank, float4 v) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_smem)), "r"(rank));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w) : "memory");
+}
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// every CTA of the cluster has finished the pass: its DSMEM stores and global V / AccBuf / stash
+// writes are visible (release / acquire at cluster scope; the cluster-scope fence also invalidates
+// L1, so the next pass's L1-allocating cp.async reads of V / AccBuf are not stale)
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+}
+
 // Location of this line inside R_k for slice parity ax.
 struct LineLoc {
   long long row;  // offset of (line, pos=0) in the slice, valid only if ok
@@ -592,19 +613,25 @@ __host__ __device__ constexpr int tma_box(int n) { return n < PTYCHO_TMA_BOX ? n
 // after griddepcontrol.wait).  PERSIST = true: one step of chain_kernel (tables and twiddles
 // already resident, probe passed in, input written by other CTAs before the grid barrier, read
 // through L2).
-template <int N, int KIND, bool PERSIST, bool TWG = false>
+// CL = true: one step of cluster_chain_kernel -- the CTA holds N/16 lines of a 16-CTA cluster as
+// groups of LINES_PER_CTA lines (tid = thread index inside the group, smem = the group's region);
+// the pass input is read from the CTA's own shared memory (cin: its N/16 lines) and the transposed
+// output is written straight into the owning CTA's shared memory over DSMEM (cout).
+template <int N, int KIND, bool PERSIST, bool TWG = false, bool CL = false>
 __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4 pd,
                                           const float2 (&twr)[EngOf<N>::type::T * EngOf<N>::type::T == N
                                                                   ? EngOf<N>::type::E : 1],
                                           unsigned char* smem, const CUtensorMap* tmV = nullptr,
-                                          const CUtensorMap* tmA = nullptr) {
+                                          const CUtensorMap* tmA = nullptr, const float2* cin = nullptr,
+                                          float2* cout = nullptr) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
   constexpr Plan PL = plan_of(KIND);
   using SM = Smem<N, KIND>;
   float2* tw = (float2*)(smem + SM::tw);
   float2* ht = (float2*)(smem + SM::ht);
-  const int lw = threadIdx.x / Q, q = threadIdx.x % Q;
+  const int tid = CL ? (int)(threadIdx.x % (L * Q)) : (int)threadIdx.x;
+  const int lw = tid / Q, q = tid % Q;
   const int bid = 1 + lw;  // named barrier of this line (engines with T > 32)
   const unsigned long long pol = l2_stream_policy();
   const int line = grp * L + lw;
@@ -622,8 +649,8 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   // tables: asynchronous copies (no register round trip); waited for with the other prefetches
   if constexpr (!PERSIST) {
     if constexpr (!TW_REG && !TWG)
-      for (int e = threadIdx.x; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
-    for (int e = threadIdx.x; e < N / 4 + 1; e += L * Q) cp_async16((float4*)ht + e, (const float4*)a.htab + e);
+      for (int e = tid; e < ENG::TW / 2; e += L * Q) cp_async16((float4*)tw + e, (const float4*)a.wtab + e);
+    for (int e = tid; e < N / 4 + 1; e += L * Q) cp_async16((float4*)ht + e, (const float4*)a.htab + e);
   }
   cp_async_commit();  // group 1: tables
   constexpr bool FIRST = kind_first(KIND);
@@ -659,36 +686,39 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   constexpr bool NEED_V = kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND);
   unsigned long long* mbar = (unsigned long long*)(smem + SM::bar);
   const int xal = LL.pos0 & ~3;                       // 16-B aligned start of the superset
+  auto lidx_of = [&](int ln) { return ax == 0 ? wy0 + ln - a.ey0 : wx0 + ln - a.ex0; };
   const int dsh = (TMA && NEED_V) ? (LL.pos0 & 3) : 0;  // shift of window position 0 in pv / pacc
   if constexpr (TMA) {
-    if (threadIdx.x == 0) {
-      mbar_init(mbar, 1);
+    // the first thread of every line issues its own line's copies (L issuers in parallel; one
+    // issuer for the whole CTA kept the other warps waiting at the next __syncthreads)
+    if (tid == 0) {
+      mbar_init(mbar, L);
       fence_proxy_async();
+    }
+    __syncthreads();
+    if (q == 0) {
       constexpr unsigned row = 4u * N + 16u;
       constexpr unsigned per = (NEED_V ? row : 0u) + (kind_grad(KIND) ? 8u * N : 0u) + (KIND == K_TURN ? 4u * N : 0u);
       const unsigned acc_bytes = (kind_grad(KIND) && !a.no_acc) ? row : 0u;
-      mbar_expect_tx(mbar, (per + acc_bytes) * L);
-      for (int l = 0; l < L; ++l) {
-        const int ln = grp * L + l;
-        const int li = ax == 0 ? wy0 + ln - a.ey0 : wx0 + ln - a.ex0;
-        unsigned char* lb = smem + SM::lines + l * SM::per_line;
-        if constexpr (NEED_V) {
-          unsigned char* d = lb + SM::ex_b + SM::st_b;
+      mbar_expect_tx(mbar, per + acc_bytes);
+      const int li = lidx_of(line);
+      unsigned char* lb = smem + SM::lines + lw * SM::per_line;
+      if constexpr (NEED_V) {
+        unsigned char* d = lb + SM::ex_b + SM::st_b;
 #pragma unroll
-          for (int b = 0; b < NBOX; ++b) tma_load3(d + b * BOX * 4, tmV, xal + b * BOX, li, a.s >> 1, mbar, pol);
-          tma_load3(d + N * 4, tmV + 4, xal + N, li, a.s >> 1, mbar, pol);  // 4-float tail box
-        }
-        if constexpr (kind_grad(KIND)) {
-          if (!a.no_acc) {
-            unsigned char* d = lb + SM::ex_b + SM::st_b + SM::v_b;
-#pragma unroll
-            for (int b = 0; b < NBOX; ++b) tma_load3(d + b * BOX * 4, tmA, xal + b * BOX, li, a.s >> 1, mbar, pol);
-            tma_load3(d + N * 4, tmA + 4, xal + N, li, a.s >> 1, mbar, pol);
-          }
-          bulk_load(lb + SM::ex_b, a.stash + (size_t)a.stash_s * N * N + (size_t)ln * N, 8u * N, mbar, pol);
-        }
-        if constexpr (KIND == K_TURN) bulk_load(lb + SM::ex_b + SM::st_b, a.amp + (size_t)i * N * N + (size_t)ln * N, 4u * N, mbar, pol);
+        for (int b = 0; b < NBOX; ++b) tma_load3(d + b * BOX * 4, tmV, xal + b * BOX, li, a.s >> 1, mbar, pol);
+        tma_load3(d + N * 4, tmV + 4, xal + N, li, a.s >> 1, mbar, pol);  // 4-float tail box
       }
+      if constexpr (kind_grad(KIND)) {
+        if (!a.no_acc) {
+          unsigned char* d = lb + SM::ex_b + SM::st_b + SM::v_b;
+#pragma unroll
+          for (int b = 0; b < NBOX; ++b) tma_load3(d + b * BOX * 4, tmA, xal + b * BOX, li, a.s >> 1, mbar, pol);
+          tma_load3(d + N * 4, tmA + 4, xal + N, li, a.s >> 1, mbar, pol);
+        }
+        bulk_load(lb + SM::ex_b, a.stash + (size_t)a.stash_s * N * N + (size_t)line * N, 8u * N, mbar, pol);
+      }
+      if constexpr (KIND == K_TURN) bulk_load(lb + SM::ex_b + SM::st_b, a.amp + (size_t)i * N * N + (size_t)line * N, 4u * N, mbar, pol);
     }
   }
   if constexpr (!TMA && (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND))) {
@@ -738,6 +768,10 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     griddep_wait();
     griddep_launch();
     const float2* src = (KIND == K_RECON_FIRST ? a.stash + (size_t)a.stash_s * N * N : a.in) + (size_t)line * N + q;
+#pragma unroll
+    for (int k = 0; k < P; ++k) x[k] = src[Q * k];
+  } else if constexpr (CL) {
+    const float2* src = cin + (size_t)(line % (N / 16)) * N + q;  // written over DSMEM by the cluster
 #pragma unroll
     for (int k = 0; k < P; ++k) x[k] = src[Q * k];
   } else {
@@ -987,11 +1021,11 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     float* red = (float*)(smem + SM::red);  // LINES_PER_CTA * Q / 32 <= 16 floats
     static_assert(LINES_PER_CTA * Q / 32 + 1 <= 16, "red");
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    if ((tid & 31) == 0) red[tid >> 5] = part;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       double tot = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += (double)red[w];
+      for (int w = 0; w < (L * Q + 31) / 32; ++w) tot += (double)red[w];
       a.loss_part[grp] += tot;
     }
   }
@@ -1016,11 +1050,16 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     __syncthreads();
     float2* dst = a.out + (size_t)grp * L;
 #pragma unroll kStoreUnroll
-    for (int e = threadIdx.x; e < N * 2; e += L * Q) {
+    for (int e = tid; e < N * 2; e += L * Q) {
       const int j = e >> 1, c = e & 1, sw = (j >> 2) & 3;
       float4 v = *(const float4*)(stg + j * 4 + 2 * c);
       if (sw & 1) v = make_float4(v.z, v.w, v.x, v.y);
-      *(float4*)(dst + (size_t)j * N + 2 * (c ^ (sw >> 1))) = v;
+      if constexpr (CL) {  // next pass's line j lives in cluster CTA j / (N/16), row j % (N/16)
+        const float2* loc = cout + (size_t)(j % (N / 16)) * N + grp * L + 2 * (c ^ (sw >> 1));
+        st_cluster_v4(loc, (unsigned)(j / (N / 16)), v);
+      } else {
+        *(float4*)(dst + (size_t)j * N + 2 * (c ^ (sw >> 1))) = v;
+      }
     }
   }
   if constexpr (STORE == 2) {
@@ -1034,7 +1073,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 
   if (!PERSIST && a.advance) {
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       __threadfence();
       const unsigned prev = atomicAdd(a.done, 1u);
       if (prev == gridDim.x - 1) {  // every CTA has read *desc: advance to the next probe
@@ -1183,6 +1222,16 @@ __global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, 2) chain_ker
 }
 
 template <int N>
+__host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+template <int N>
+__host__ __device__ constexpr size_t chain_smem_max() {
+  return cmax<N>(cmax<N>(cmax<N>(Smem<N, K_FWD_FIRST_PROP>::alloc, Smem<N, K_FWD_FIRST_FFT>::alloc),
+                         cmax<N>(Smem<N, K_FWD_MID>::alloc, Smem<N, K_FWD_LAST>::alloc)),
+                 cmax<N>(cmax<N>(Smem<N, K_TURN>::alloc, Smem<N, K_BWD_LAST_PROP>::alloc),
+                         cmax<N>(cmax<N>(Smem<N, K_BWD_LAST_END>::alloc, Smem<N, K_BWD_MID>::alloc),
+                                 Smem<N, K_BWD_END>::alloc)));
+}
+template <int N>
 static size_t chain_smem() {
   size_t m = 0;
   const size_t v[] = {Smem<N, K_FWD_FIRST_PROP>::alloc, Smem<N, K_FWD_FIRST_FFT>::alloc, Smem<N, K_FWD_MID>::alloc,
@@ -1217,6 +1266,106 @@ cudaError_t launch_chain(int n, const ChainArgs& c, cudaStream_t stream) {
     case 64: return launch_chain_n<64>(c, stream);
     case 256: return launch_chain_n<256>(c, stream);
     case 1024: return launch_chain_n<1024>(c, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Cluster-resident chain for N <= 256 (SURVEY §7 phase 7): one 16-CTA cluster per tile runs the
+// whole probe chain of a pass segment in one launch.  The N x N wavefield never leaves the
+// cluster: CTA r holds lines [r N/16, (r+1) N/16) in shared memory (double buffered), each pass
+// writes its transposed output straight into the owning CTA's buffer over DSMEM, and a cluster
+// barrier replaces the kernel boundary of the graph + PDL chain (whose launch / prologue /
+// grid-completion latency dominates the small passes: 3.9 us per N = 256 pass).  The arithmetic
+// of every pass is pass_body's, so results are bit-identical to the standalone chain.
+// ------------------------------------------------------------------------------------------
+template <int N>
+struct ClusterLayout {
+  static constexpr int LPC = N / 16;                    // lines per CTA
+  static constexpr int G = LPC / LINES_PER_CTA;         // pass_body groups per CTA
+  static constexpr int TPG = LINES_PER_CTA * EngThreads<N>::v;
+  static constexpr size_t wbuf = (size_t)LPC * N * 8;   // one wavefield buffer (bytes)
+  static constexpr size_t group = (chain_smem_max<N>() + 127) / 128 * 128;
+  static constexpr size_t total = 2 * wbuf + G * group;
+};
+
+template <int N>
+__global__ void __launch_bounds__(ClusterLayout<N>::G * ClusterLayout<N>::TPG, 1) cluster_chain_kernel(const ChainArgs c) {
+  using CLY = ClusterLayout<N>;
+  using ENG = typename EngOf<N>::type;
+  constexpr int P = ENG::E, Q = ENG::T;
+  static_assert(ENG::T * ENG::T == N, "four-step engine (twiddles in registers)");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const unsigned rank = cluster_ctarank();
+  const int tl = blockIdx.x / 16;
+  const int g = threadIdx.x / CLY::TPG, tid = threadIdx.x % CLY::TPG, q = tid % Q;
+  unsigned char* gsm = smem + 2 * CLY::wbuf + g * CLY::group;
+  float2* wb[2] = {(float2*)smem, (float2*)(smem + CLY::wbuf)};
+  const PassArgs& a0 = c.t[tl];
+  float2 twr[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) twr[k] = __ldg(a0.wtab + k * Q + q);
+  {
+    float2* ht = (float2*)(gsm + Smem<N, K_FWD_MID>::ht);
+    for (int e = tid; e <= N / 2; e += CLY::TPG) ht[e] = a0.htab[e];
+  }
+  __syncthreads();
+  PassArgs a = a0;
+  const int S = c.S, cnt = c.count[tl];
+  const int grp = (int)rank * CLY::G + g;
+  for (int j = 0; j < cnt; ++j) {
+    const int pi = c.first + j;
+    const int2 ctr = a.centers[pi];
+    const int4 pd = make_int4(pi, ctr.x - N / 2, ctr.y - N / 2, 0);
+    for (int pp = 0; pp < 2 * S + 1; ++pp) {
+      const int kind = chain_kind(pp, S), sl = chain_slice(pp, S);
+      a.s = sl;
+      a.stash_s = sl;
+      a.stash_store = 1;
+      const float2* cin = wb[pp & 1];
+      float2* cout = wb[(pp + 1) & 1];
+      switch (kind) {
+        case K_FWD_FIRST_PROP: pass_body<N, K_FWD_FIRST_PROP, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        case K_FWD_FIRST_FFT: pass_body<N, K_FWD_FIRST_FFT, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        case K_FWD_MID: pass_body<N, K_FWD_MID, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        case K_FWD_LAST: pass_body<N, K_FWD_LAST, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        case K_TURN: pass_body<N, K_TURN, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        case K_BWD_LAST_PROP: pass_body<N, K_BWD_LAST_PROP, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        case K_BWD_LAST_END: pass_body<N, K_BWD_LAST_END, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        case K_BWD_MID: pass_body<N, K_BWD_MID, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+        default: pass_body<N, K_BWD_END, true, false, true>(a, grp, pd, twr, gsm, nullptr, nullptr, cin, cout); break;
+      }
+      cluster_sync_all();
+    }
+  }
+}
+
+template <int N>
+static cudaError_t launch_cluster_n(const ChainArgs& c, cudaStream_t stream) {
+  using CLY = ClusterLayout<N>;
+  auto kern = cluster_chain_kernel<N>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CLY::total);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16 * c.ntiles);
+  cfg.blockDim = dim3(CLY::G * CLY::TPG);
+  cfg.dynamicSmemBytes = CLY::total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 16;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, c);
+}
+
+cudaError_t launch_cluster(int n, const ChainArgs& c, cudaStream_t stream) {
+  switch (n) {
+    case 64: return launch_cluster_n<64>(c, stream);
+    case 256: return launch_cluster_n<256>(c, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -28,10 +28,13 @@ def problem():
     return n, s, h, w, sigma, c, probe, vt, centers, amps
 
 
-def run(grid, owner, nid, rank, world, device, iters=2, period=0):
+def run(grid, owner, nid, rank, world, device, iters=2, period=0, hve=False):
     n, s, h, w, sigma, c, probe, vt, centers, amps = problem()
-    p = Ptycho(n, s, h, w, sigma, c, alpha=1.0, pass_period=period, device=device)
-    p.set_tiles(grid[0], grid[1], n // 2, owner, nid, rank, world)
+    p = Ptycho(n, s, h, w, sigma, c, alpha=1.0, alpha_acc=0.0 if hve else None, pass_period=period, device=device)
+    if hve:  # Halo Voxel Exchange baseline: V copy-paste messages between ranks (NCCL)
+        p.set_tiles_hve(grid[0], grid[1], 24, 25, owner, nid, rank, world)
+    else:
+        p.set_tiles(grid[0], grid[1], n // 2, owner, nid, rank, world)
     p.set_scan(centers)
     p.allocate_workspace()
     p.set_probe(probe.astype(np.complex64))
@@ -66,6 +69,18 @@ def main():
             same = np.array_equal(multi, single) and lm == ls
             print(f"grid {grid} T={period} transport {tr}: multi-GPU == single-GPU virtual tiles: {same}; "
                   f"losses {lm} {ls}", flush=True)
+            ok &= same
+        dist.barrier()
+    for grid in [(2, 3), (2, 2)]:
+        nt = grid[0] * grid[1]
+        owner = [k * world // nt for k in range(nt)]
+        obj = [Ptycho.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        multi, lm, _ = run(grid, owner, obj[0], rank, world, local, hve=True)
+        if rank == 0:
+            single, ls, _ = run(grid, None, None, 0, 1, local, hve=True)
+            same = np.array_equal(multi, single) and lm == ls
+            print(f"HVE grid {grid}: multi-GPU == single-GPU virtual tiles: {same}; losses {lm} {ls}", flush=True)
             ok &= same
         dist.barrier()
     # APPP integer bit-exactness across ranks

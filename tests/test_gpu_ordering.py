@@ -9,7 +9,9 @@ is closed on this pool, so two checks of our own:
    1024.  The bits must be 0 and the results bit-identical to the product library.
 2. Launch-mode invariance of the product library: graph + PDL (default), PDL off
    (PTYCHO_NO_PDL=1: every pass fully serialised after the previous one), graphs off
-   (PTYCHO_NO_GRAPH=1) -- a race in the pre-wait prefetch would make these differ.
+   (PTYCHO_NO_GRAPH=1), and for N <= 256 the opt-in cluster-resident chain (PTYCHO_CLUSTER=1:
+   wavefield exchanged over DSMEM, cluster barriers instead of kernel boundaries) -- a race in the
+   pre-wait prefetch or in the DSMEM exchange would make these differ.
 """
 import json
 import os
@@ -47,7 +49,7 @@ def test_debug_checks_see_no_stale_prefetch(product):
         assert dbg[name]["sha"] == product[name]["sha"], name  # the checks only read
 
 
-@pytest.mark.parametrize("mode", [{"PTYCHO_NO_PDL": "1"}, {"PTYCHO_NO_GRAPH": "1"}])
+@pytest.mark.parametrize("mode", [{"PTYCHO_NO_PDL": "1"}, {"PTYCHO_NO_GRAPH": "1"}, {"PTYCHO_CLUSTER": "1"}])
 def test_launch_mode_invariance(product, mode):
     other = _run(mode)
     for name in CASES:
