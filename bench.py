@@ -336,8 +336,15 @@ def main():
     appp = None
     if world > 1:
         from paper_2205_06327_b200.ptycho import appp_schedule
-        xbytes = sum((y1 - y0) * (x1 - x0) * S * 4 for (a, b, y0, y1, x0, x1, _) in appp_schedule(H, W, R, C, halo)
+        sched = appp_schedule(H, W, R, C, halo)
+        xbytes = sum((y1 - y0) * (x1 - x0) * S * 4 for (a, b, y0, y1, x0, x1, _) in sched
                      if owner[a] != owner[b] and y1 > y0 and x1 > x0)
+        # bytes each rank receives over NVLink in one call (its hops run in order on its stream):
+        # the busiest receiver's bytes / call time = the rate of an active link
+        recv = [0] * world
+        for (a, b, y0, y1, x0, x1, _) in sched:
+            if owner[a] != owner[b] and y1 > y0 and x1 > x0:
+                recv[owner[b]] += (y1 - y0) * (x1 - x0) * S * 4
         for _ in range(2):
             p.appp_passes()
         barrier()
@@ -353,6 +360,8 @@ def main():
         ams = float(t.item())
         appp = {"transport": p.appp_transport(), "ms_per_call": ams, "cross_rank_bytes": xbytes,
                 "achieved_gbs_per_gpu": xbytes / world / (ams * 1e6), "nvlink_peak_gbs_per_gpu": 900.0,
+                "busiest_receiver_bytes": max(recv), "achieved_gbs_busiest_receiver": max(recv) / (ams * 1e6),
+                "frac_of_nvlink_busiest_receiver": max(recv) / (ams * 1e6) / 900.0,
                 "note": "not pipelined behind the backward here; in ptycho_iterate the slabs overlap it"}
 
     # ---- roofline of the dominant kernel (backward middle pass), CUDA events on its stream

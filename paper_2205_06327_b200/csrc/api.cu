@@ -142,7 +142,8 @@ struct ptycho_ctx_s {
   unsigned* p2p_err = nullptr;                  // pinned, mapped: a P2P flag wait timed out
   unsigned* p2p_err_dev = nullptr;
   unsigned long long p2p_timeout_ns = 600ull * 1000000000ull;
-  std::vector<cudaEvent_t>* wait_ev = nullptr;  // ptycho_profile_iteration: events around P2P waits
+  std::vector<cudaEvent_t>* wait_ev = nullptr;    // ptycho_profile_iteration: events around P2P waits
+  std::vector<cudaEvent_t>* signal_ev = nullptr;  // ... and around the senders' READY -> DONE spins
 };
 
 static thread_local std::string g_create_err;
@@ -1407,8 +1408,17 @@ static ptycho_status hop_p2p(ptycho_ctx ctx, const Hop& h, size_t hid, bool send
     return (unsigned*)(ctx->peer_ws[r] + ctx->peer_flags[r]) + which * nh + hid;
   };
   if (sender) {
+    cudaEvent_t s0 = nullptr, s1 = nullptr;
+    if (ctx->signal_ev) {
+      CK(cudaEventCreate(&s0));
+      CK(cudaEventCreate(&s1));
+      ctx->signal_ev->push_back(s0);
+      ctx->signal_ev->push_back(s1);
+      CK(cudaEventRecord(s0, ctx->stream));
+    }
     CK(launch_p2p_signal(peer_flag(b.owner, 0), ep, ctx->flags + nh + hid, ctx->p2p_timeout_ns, ctx->p2p_err_dev,
                          ctx->stream));
+    if (s1) CK(cudaEventRecord(s1, ctx->stream));
     ++ctx->launches;
     return PTYCHO_OK;
   }
@@ -1644,18 +1654,19 @@ extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out
   if (!ms_out) return fail(ctx, PTYCHO_EARG, "ms_out is NULL");
   if (ctx->hve) return fail(ctx, PTYCHO_ESTATE, "profile_iteration: GD contexts only");
   CK(cudaSetDevice(ctx->device));
-  for (int i = 0; i < 5; ++i) ms_out[i] = 0.0;
+  for (int i = 0; i < 6; ++i) ms_out[i] = 0.0;
   size_t nmax = 0;
   for (const Tile& t : ctx->tiles) nmax = std::max(nmax, t.probes.size());
   if (nmax == 0) return PTYCHO_OK;
   const int64_t T = ctx->cfg.pass_period > 0 ? ctx->cfg.pass_period : (int64_t)nmax;
   const int64_t nseg = ((int64_t)nmax + T - 1) / T;
-  std::vector<cudaEvent_t> ev(4 * nseg + 1, nullptr), wait_ev;
+  std::vector<cudaEvent_t> ev(4 * nseg + 1, nullptr), wait_ev, signal_ev;
   for (auto& e : ev) CK(cudaEventCreate(&e));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaEventRecord(ev[0], ctx->stream));
   ptycho_status st = PTYCHO_OK;
   ctx->wait_ev = &wait_ev;
+  ctx->signal_ev = &signal_ev;
   for (int64_t j = 0; j < nseg && st == PTYCHO_OK; ++j) {
     if (j) CK(cudaEventRecord(ev[4 * j], ctx->stream));
     st = run_probes(ctx, j * T, T, CHAIN_GRAD);
@@ -1666,6 +1677,7 @@ extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out
     if (st == PTYCHO_OK) st = cudaEventRecord(ev[4 * j + 3], ctx->stream) == cudaSuccess ? PTYCHO_OK : PTYCHO_ECUDA;
   }
   ctx->wait_ev = nullptr;
+  ctx->signal_ev = nullptr;
   if (st == PTYCHO_OK) {
     CK(cudaEventRecord(ev[4 * nseg], ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1686,10 +1698,15 @@ extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out
       CK(cudaEventElapsedTime(&ms, wait_ev[i], wait_ev[i + 1]));
       ms_out[2] += ms;
     }
-    ms_out[3] = std::max(0.0, appp - ms_out[2]);
+    for (size_t i = 0; i + 1 < signal_ev.size(); i += 2) {
+      CK(cudaEventElapsedTime(&ms, signal_ev[i], signal_ev[i + 1]));
+      ms_out[5] += ms;
+    }
+    ms_out[3] = std::max(0.0, appp - ms_out[2] - ms_out[5]);
   }
   for (auto e : ev) cudaEventDestroy(e);
   for (auto e : wait_ev) cudaEventDestroy(e);
+  for (auto e : signal_ev) cudaEventDestroy(e);
   return st == PTYCHO_OK ? PTYCHO_OK : (ctx->err.empty() ? fail(ctx, st, "profile_iteration failed") : st);
 }
 
