@@ -250,8 +250,8 @@ def main():
                     help="stash-free adjoint (PTYCHO_F_STASH_FREE): phi_s recomputed, 2-slice stash")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-async", choices=["auto", "on", "off"], default="auto",
-                    help="e2e: PTYCHO_AMP_ASYNC load overlapping the chains; auto = on at >= 4 GPUs, "
-                         "where the ranks share the host's upload bandwidth (N=4: e2e +16 %%), off "
+                    help="e2e: PTYCHO_AMP_ASYNC load overlapping the chains; auto = on at >= 4 ranks per "
+                         "host, where they share its upload bandwidth (N=4: e2e +16 %%), off "
                          "below (N=1: -2.5 %%, N=2: -8 %%); profiles/round1.md")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -457,7 +457,8 @@ def main():
     # ---- e2e: host measurements (pinned) -> device, one iteration, stitched V -> host, each step
     e2e = None
     if not args.no_e2e:
-        e2e_async = args.e2e_async == "on" or (args.e2e_async == "auto" and world >= 4)
+        # the rationale is the host's shared upload bandwidth: ranks per HOST, not world size
+        e2e_async = args.e2e_async == "on" or (args.e2e_async == "auto" and env_int("LOCAL_WORLD_SIZE", world) >= 4)
         host_amp = torch.empty((nloc, n, n), dtype=torch.float32, pin_memory=True)
         p.read_measurements(0, nloc, host_amp)
         host_v = torch.empty((S, H, W), dtype=torch.float32, pin_memory=True) if rank == 0 else None

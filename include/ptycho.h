@@ -69,8 +69,10 @@ typedef enum {
                                  /* overlaps the gradient passes.  The host buffer (pinned for real  */
                                  /* asynchrony) must stay valid and unchanged until                  */
                                  /* ptycho_synchronize.  Otherwise the flag is ignored (synchronous). */
-                                 /* Measured on B200 (LT-small, 8 tiles): the overlapped copy slows  */
-                                 /* the chains by more than it saves (10.09 vs 9.84 s per e2e step). */
+                                 /* Measured on B200, LT-small: with one rank per host the overlapped */
+                                 /* copy slows the chains by more than it saves (1 and 2 GPUs); with  */
+                                 /* 4 ranks sharing the host's upload bandwidth it wins (+16 % e2e),  */
+                                 /* so bench.py enables it at >= 4 ranks per host (LOCAL_WORLD_SIZE). */
 
 typedef struct {
   int32_t n;         /* N: probe window = detector side; 64, 256 or 1024                          */

@@ -401,12 +401,19 @@ def test_async_measurement_load_bit_identical(batched):
         for hb in (h1, h2, h1):
             p.load_measurements(hb, flags=flags)
             losses.append(p.iterate(want_loss=True))
+        # loads of different data with NO synchronisation in between (iterate without
+        # the loss returns with the chains still queued), so a load is enqueued while the previous
+        # iteration's chains may still read the stores it overwrites
+        for hb in (h2, h1, h2):
+            p.load_measurements(hb, flags=flags)
+            p.iterate()
+        p.synchronize()
         back = np.zeros_like(amps[ids])
         p.read_measurements(0, len(ids), back)
         outs.append((p.stitch(), losses, back))
         p.close()
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
-    assert np.array_equal(outs[1][2], amps[ids])
+    assert np.array_equal(outs[1][2], amps2[ids])
 
 
 def test_global_probe_exports_match_tile_exports():
