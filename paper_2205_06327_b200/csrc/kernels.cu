@@ -196,6 +196,47 @@ struct EngFour {
     }
     __syncwarp();
   }
+  // the same transpose through a real-valued buffer of half the size (rows padded to P + 4 floats:
+  // STS.32 column writes and LDS.128 row reads conflict-free), real parts then imaginary parts --
+  // for the 3-CTA/SM backward build, where shared memory is the occupancy limit
+  static constexpr int LDH = P + 4;
+  static constexpr int EXH = P * LDH;  // floats
+  __device__ __forceinline__ static void exchange_half(float2 (&x)[E], float* __restrict__ exf, int q) {
+    const float4* row = (const float4*)(exf + q * LDH);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < P; ++k) exf[k * LDH + q] = x[k].x;
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < P / 4; ++n) {
+      const float4 v = row[n];
+      x[4 * n].x = v.x;
+      x[4 * n + 1].x = v.y;
+      x[4 * n + 2].x = v.z;
+      x[4 * n + 3].x = v.w;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < P; ++k) exf[k * LDH + q] = x[k].y;
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < P / 4; ++n) {
+      const float4 v = row[n];
+      x[4 * n].y = v.x;
+      x[4 * n + 1].y = v.y;
+      x[4 * n + 2].y = v.z;
+      x[4 * n + 3].y = v.w;
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ static void fft_rh(float2 (&x)[E], float* __restrict__ exf, int q,
+                                               const float2 (&twr)[P]) {
+    DftReg<P>::run(x);
+#pragma unroll
+    for (int k = 1; k < P; ++k) x[k] = cmul(x[k], twr[k]);
+    exchange_half(x, exf, q);
+    DftReg<P>::run(x);
+  }
   __device__ __forceinline__ static void fft(float2 (&x)[E], float2* __restrict__ ex, int q,
                                             const float2* __restrict__ tw) {
     DftReg<P>::run(x);
@@ -502,6 +543,17 @@ __device__ __forceinline__ void st_stream(float2* p, float2 v, unsigned long lon
   *p = v;
 #endif
 }
+// AccBuf_k[p] += g (Alg. 1 step 7) as a fire-and-forget L2 reduction: one writer per voxel per
+// probe and probes are stream-ordered, so the result is fl(AccBuf + g) exactly as a read-modify-
+// write -- without the prefetch of the AccBuf row (4 KB of shared memory per line at N = 1024) and
+// without the load latency
+__device__ __forceinline__ void red_add_stream(float* p, float v, unsigned long long pol) {
+#ifndef PTYCHO_NO_L2_HINTS
+  asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+#else
+  atomicAdd(p, v);
+#endif
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -578,8 +630,8 @@ __device__ __forceinline__ LineLoc line_loc(const PassArgs& a, int ax, int line,
   return L;
 }
 
-// Shared-memory carve-up of a pass CTA.
-template <int N, int KIND>
+// Shared-memory carve-up of a pass CTA.  HALF: the half-size exchange buffer (EngFour only).
+template <int N, int KIND, bool HALF = false>
 struct Smem {
   using ENG = typename EngOf<N>::type;
   static constexpr int L = LINES_PER_CTA;
@@ -589,13 +641,18 @@ struct Smem {
   static constexpr size_t bar = ht + (N / 2 + 2) * 8;                // mbarrier of the TMA prefetch
   static constexpr size_t red = bar + 8;                             // TURN: per-warp loss partials
   static constexpr size_t lines = (red + 64 + 127) / 128 * 128;      // per-line buffers, 128-B aligned (TMA)
-  static constexpr size_t ex_b = (size_t)ENG::EX * 8;                // exchange buffer per line
+  static constexpr size_t ex_b = HALF ? ((size_t)ENG::T * (ENG::T + 4) * 4 + 127) / 128 * 128
+                                      : (size_t)ENG::EX * 8;          // exchange buffer per line
   static constexpr size_t st_b = kind_grad(KIND) ? (size_t)N * 8 : 0;  // stash prefetch per line
   // V / AccBuf rows: N floats + the 4-float tail of the 16-B aligned TMA superset (rounded to
   // 128 B so that every TMA destination stays 128-B aligned)
   static constexpr size_t v_b =
       (kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND) || KIND == K_TURN) ? (size_t)N * 4 + 128 : 0;
+#ifdef PTYCHO_ACC_RMW
   static constexpr size_t acc_b = kind_grad(KIND) ? (size_t)N * 4 + 128 : 0;  // AccBuf prefetch per line
+#else
+  static constexpr size_t acc_b = 0;  // AccBuf += g by red.global.add: no prefetch, no buffer
+#endif
   static constexpr size_t per_line = ex_b + st_b + v_b + acc_b;
   static constexpr size_t stage_b = (size_t)N * (L + 1) * 8;         // transposed-store staging
   static constexpr size_t total = lines + (per_line * L > stage_b ? per_line * L : stage_b);
@@ -617,7 +674,7 @@ __host__ __device__ constexpr int tma_box(int n) { return n < PTYCHO_TMA_BOX ? n
 // groups of LINES_PER_CTA lines (tid = thread index inside the group, smem = the group's region);
 // the pass input is read from the CTA's own shared memory (cin: its N/16 lines) and the transposed
 // output is written straight into the owning CTA's shared memory over DSMEM (cout).
-template <int N, int KIND, bool PERSIST, bool TWG = false, bool CL = false>
+template <int N, int KIND, bool PERSIST, bool TWG = false, bool CL = false, bool HALF = false>
 __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4 pd,
                                           const float2 (&twr)[EngOf<N>::type::T * EngOf<N>::type::T == N
                                                                   ? EngOf<N>::type::E : 1],
@@ -627,7 +684,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T, L = LINES_PER_CTA;
   constexpr Plan PL = plan_of(KIND);
-  using SM = Smem<N, KIND>;
+  using SM = Smem<N, KIND, HALF>;
   float2* tw = (float2*)(smem + SM::tw);
   float2* ht = (float2*)(smem + SM::ht);
   const int tid = CL ? (int)(threadIdx.x % (L * Q)) : (int)threadIdx.x;
@@ -699,7 +756,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     if (q == 0) {
       constexpr unsigned row = 4u * N + 16u;
       constexpr unsigned per = (NEED_V ? row : 0u) + (kind_grad(KIND) ? 8u * N : 0u) + (KIND == K_TURN ? 4u * N : 0u);
-      const unsigned acc_bytes = (kind_grad(KIND) && !a.no_acc) ? row : 0u;
+      const unsigned acc_bytes = (kind_grad(KIND) && SM::acc_b && !a.no_acc) ? row : 0u;
       mbar_expect_tx(mbar, per + acc_bytes);
       const int li = lidx_of(line);
       unsigned char* lb = smem + SM::lines + lw * SM::per_line;
@@ -710,7 +767,7 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         tma_load3(d + N * 4, tmV + 4, xal + N, li, a.s >> 1, mbar, pol);  // 4-float tail box
       }
       if constexpr (kind_grad(KIND)) {
-        if (!a.no_acc) {
+        if (SM::acc_b && !a.no_acc) {
           unsigned char* d = lb + SM::ex_b + SM::st_b + SM::v_b;
 #pragma unroll
           for (int b = 0; b < NBOX; ++b) tma_load3(d + b * BOX * 4, tmA, xal + b * BOX, li, a.s >> 1, mbar, pol);
@@ -730,12 +787,12 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       const int j = q + Q * k, p = LL.pos0 + j;
       if (LL.ok && (unsigned)p < (unsigned)LL.plim) {
         cp_async4s(pv + j, vrow + p, pol);
-        if constexpr (kind_grad(KIND)) {
+        if constexpr (kind_grad(KIND) && SM::acc_b > 0) {
           if (!a.no_acc) cp_async4s(pacc + j, arow + p, pol);
         }
       } else {
         pv[j] = 0.f;
-        if constexpr (kind_grad(KIND)) pacc[j] = 0.f;
+        if constexpr (kind_grad(KIND) && SM::acc_b > 0) pacc[j] = 0.f;
       }
     }
   }
@@ -919,14 +976,16 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
       ENG::sync_line(bid);
       const float two_sigma = 2.0f * a.sigma;
       const bool exporting = a.gexport != nullptr;  // debug: write g instead of updating
+      float* gexp = exporting ? a.gexport + (size_t)a.s * N * N : nullptr;
       const int lim = LL.ok ? LL.plim : 0;
 #ifndef PTYCHO_UNROLLED_STEPS
       // Rolled over the line through the (idle) exchange buffer: the unrolled body was ~13 KB of
       // SASS, and the pass loop (transform + steps) then overflowed the 32 KB instruction cache.
       // Each thread only touches its own positions, so no synchronisation is needed.
       float2* xs = ex;
-#pragma unroll
-      for (int k = 0; k < P; ++k) xs[ENG::idx(dist, q, k)] = x[k];
+      // HALF (3-CTA/SM backward build): the exchange buffer holds half a line of complex values,
+      // so the line is rolled through it in two halves of the thread's elements
+      constexpr int NH = HALF ? 2 : 1, KH = P / NH;
 #ifdef PTYCHO_DEBUG_CHECKS
       {  // V / AccBuf / stash rows prefetched before griddepcontrol.wait equal their L2 values now
         const float2* sr = a.stash + (size_t)a.stash_s * N * N + (size_t)line * N;
@@ -935,37 +994,48 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
           const int p = LL.pos0 + j;
           if ((unsigned)p < (unsigned)lim) {
             if (__ldcg(vrow + p) != pv[j]) atomicOr(a.dbg, 1u);
-            if (!a.no_acc && __ldcg(arow + p) != pacc[j]) atomicOr(a.dbg, 2u);
+            if (SM::acc_b && !a.no_acc && __ldcg(arow + p) != pacc[j]) atomicOr(a.dbg, 2u);
           }
           const float2 sg = __ldcg(sr + j);
           if (sg.x != pst[j].x || sg.y != pst[j].y) atomicOr(a.dbg, 4u);
         }
       }
 #endif
-      auto body = [&](auto fast) {
-#pragma unroll kStepUnroll
-        for (int k = 0; k < P; ++k) {
-          const int j = ENG::idx(dist, q, k);
-          const int p = LL.pos0 + j;
-          const float2 ph = pst[j];
-          const float2 y = xs[j];
-          const float2 chi = make_float2(y.x, -y.y);
-          const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
-          const float v = pv[j];
-          if (!exporting && (unsigned)p < (unsigned)lim) {
-            if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
-            st_stream(vrow + p, v - a.alpha * g, pol);
-          }
-          pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
-          float sn, cs;
-          sincos_t<decltype(fast)::value>(a.sigma * v, &sn, &cs);
-          xs[j] = cmulc(chi, make_float2(cs, sn));
-        }
-      };
-      if (small_phases<P>(pv, a.sigma, [&](int k) { return ENG::idx(dist, q, k); })) body(Bool<true>());
-      else body(Bool<false>());
+      const bool fast_phase = small_phases<P>(pv, a.sigma, [&](int k) { return ENG::idx(dist, q, k); });
 #pragma unroll
-      for (int k = 0; k < P; ++k) x[k] = xs[ENG::idx(dist, q, k)];
+      for (int h = 0; h < NH; ++h) {
+        const int kb = h * KH, jb = HALF ? ENG::idx(dist, 0, kb) : 0;  // EngFour: j = q + Q k
+#pragma unroll
+        for (int k = kb; k < kb + KH; ++k) xs[ENG::idx(dist, q, k) - jb] = x[k];
+        auto body = [&](auto fast) {
+#pragma unroll kStepUnroll
+          for (int k = kb; k < kb + KH; ++k) {
+            const int j = ENG::idx(dist, q, k);
+            const int p = LL.pos0 + j;
+            const float2 ph = pst[j];
+            const float2 y = xs[j - jb];
+            const float2 chi = make_float2(y.x, -y.y);
+            const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
+            const float v = pv[j];
+            if (!exporting && (unsigned)p < (unsigned)lim) {
+              if constexpr (SM::acc_b > 0) {
+                if (!a.no_acc) st_stream(arow + p, pacc[j] + g, pol);
+              } else {
+                if (!a.no_acc) red_add_stream(arow + p, g, pol);
+              }
+              st_stream(vrow + p, v - a.alpha * g, pol);
+            }
+            if (exporting) gexp[ax == 0 ? (size_t)line * N + j : (size_t)j * N + line] = g;  // debug: g itself
+            float sn, cs;
+            sincos_t<decltype(fast)::value>(a.sigma * v, &sn, &cs);
+            xs[j - jb] = cmulc(chi, make_float2(cs, sn));
+          }
+        };
+        if (fast_phase) body(Bool<true>());
+        else body(Bool<false>());
+#pragma unroll
+        for (int k = kb; k < kb + KH; ++k) x[k] = xs[ENG::idx(dist, q, k) - jb];
+      }
 #else
 #pragma unroll
       for (int k = 0; k < P; ++k) {
@@ -977,24 +1047,16 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
         const float g = two_sigma * (chi.y * ph.x - chi.x * ph.y);
         const float v = pv[j];
         if (!exporting && (unsigned)p < (unsigned)lim) {
-          if (!a.no_acc) arow[p] = pacc[j] + g;
+          if (!a.no_acc) red_add_stream(arow + p, g, pol);
           vrow[p] = v - a.alpha * g;
         }
-        pacc[j] = g;  // the prefetched AccBuf word is dead: keep g for the debug export
+        if (exporting) gexp[ax == 0 ? (size_t)line * N + j : (size_t)j * N + line] = g;
         float sn, cs;
         sincos_t<false>(a.sigma * v, &sn, &cs);
         x[k] = cmulc(chi, make_float2(cs, sn));
       }
 #endif
-      if (exporting) {
-        ENG::sync_line(bid);
-        float* o = a.gexport + (size_t)a.s * N * N;
-#pragma unroll 4
-        for (int k = 0; k < P; ++k) {
-          const int j = q + Q * k;
-          o[ax == 0 ? (size_t)line * N + j : (size_t)j * N + line] = pacc[j];
-        }
-      }
+
     }
   };
 
@@ -1005,7 +1067,9 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     if (f == 2) st = PL.pre[2];
     if (f == 3) st = PL.pre[3];
     step(st, f & 1);
-    if constexpr (TW_REG) {
+    if constexpr (HALF) {
+      ENG::fft_rh(x, (float*)ex, q, twr);
+    } else if constexpr (TW_REG) {
       ENG::fft_r(x, ex, q, twr);
     } else {
       const float2* twp = TWG ? a.wtab : tw;
@@ -1092,11 +1156,26 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 // <= 168 registers leave room for CTAs of other tiles' chains (2 chains +4 %, 8 tiles +6 %
 // probes/s, but a lone chain runs 12 % slower).  The host picks per context (api.cu).  Backward
 // passes always use 2 (they spill at 168).  Both builds execute the same arithmetic.
+// HALF_BWD (opt-in, -DPTYCHO_BWD3=1): backward passes of the multi-chain build (MINB >= 3) at
+// N = 1024 at 3 CTAs/SM -- half-size exchange buffer (exchange_half), AccBuf by red.global.add and
+// the gradient step rolled in two halves bring the CTA to 72 KB of shared memory and 168
+// registers.  Bit-identical, but measured 2 % slower than 2 CTAs/SM (548 vs 560 probe-loc/s,
+// profiles/round2/ab_bwd3.txt): the extra warps do not pay for the second exchange round and
+// the register cap.
+#ifndef PTYCHO_BWD3
+#define PTYCHO_BWD3 0
+#endif
 template <int N, int KIND, int MINB>
-__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v, kind_grad(KIND) ? 2 : MINB)
+__host__ __device__ constexpr bool half_bwd() {
+  return PTYCHO_BWD3 && kind_grad(KIND) && MINB >= 3 && N == 1024 && EngOf<N>::type::T * EngOf<N>::type::T == N;
+}
+template <int N, int KIND, int MINB>
+__global__ void __launch_bounds__(LINES_PER_CTA * EngThreads<N>::v,
+                                  kind_grad(KIND) ? (half_bwd<N, KIND, MINB>() ? 3 : 2) : MINB)
 pass_kernel(const PassArgs a) {
   using ENG = typename EngOf<N>::type;
   constexpr int P = ENG::E, Q = ENG::T;
+  constexpr bool HB = half_bwd<N, KIND, MINB>();
   constexpr bool TWG = MINB >= 4 && !kind_grad(KIND) && ENG::T * ENG::T == N;
   constexpr bool TW_REG = (ENG::T * ENG::T == N) && !TWG;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1112,7 +1191,7 @@ pass_kernel(const PassArgs a) {
   constexpr int groups = N / LINES_PER_CTA;
   const int b = blockIdx.x / groups, grp = blockIdx.x - b * groups;
   if (b == 0) {
-    pass_body<N, KIND, false, TWG>(a, grp, make_int4(0, 0, 0, 0), twr, smem, a.tmV, a.tmA);
+    pass_body<N, KIND, false, TWG, false, HB>(a, grp, make_int4(0, 0, 0, 0), twr, smem, a.tmV, a.tmA);
   } else {
     PassArgs ab = a;
     ab.stash += b * a.stash_slot;
@@ -1120,7 +1199,7 @@ pass_kernel(const PassArgs a) {
     ab.out += b * a.wf_slot;
     ab.desc += b;
     ab.loss_part += b * groups;
-    pass_body<N, KIND, false, TWG>(ab, grp, make_int4(0, 0, 0, 0), twr, smem, a.tmV, a.tmA);
+    pass_body<N, KIND, false, TWG, false, HB>(ab, grp, make_int4(0, 0, 0, 0), twr, smem, a.tmV, a.tmA);
   }
 }
 
@@ -1373,7 +1452,7 @@ cudaError_t launch_cluster(int n, const ChainArgs& c, cudaStream_t stream) {
 template <int N, int KIND, int MINB>
 static cudaError_t launch_one(const PassArgs& a, cudaStream_t stream, bool pdl) {
   auto kern = pass_kernel<N, KIND, MINB>;
-  const size_t smem = Smem<N, KIND>::alloc;
+  const size_t smem = Smem<N, KIND, half_bwd<N, KIND, MINB>()>::alloc;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1402,10 +1481,10 @@ static cudaError_t launch_pass_nm(PassKind kind, const PassArgs& a, cudaStream_t
     case K_FWD_LAST: return launch_one<N, K_FWD_LAST, MINB>(a, s, pdl);
     case K_TURN: return launch_one<N, K_TURN, MINB>(a, s, pdl);
     case K_SIMULATE: return launch_one<N, K_SIMULATE, MINB>(a, s, pdl);
-    case K_BWD_LAST_PROP: return launch_one<N, K_BWD_LAST_PROP, 2>(a, s, pdl);
-    case K_BWD_LAST_END: return launch_one<N, K_BWD_LAST_END, 2>(a, s, pdl);
-    case K_BWD_MID: return launch_one<N, K_BWD_MID, 2>(a, s, pdl);
-    case K_BWD_END: return launch_one<N, K_BWD_END, 2>(a, s, pdl);
+    case K_BWD_LAST_PROP: return launch_one<N, K_BWD_LAST_PROP, (MINB >= 3 ? 3 : 2)>(a, s, pdl);
+    case K_BWD_LAST_END: return launch_one<N, K_BWD_LAST_END, (MINB >= 3 ? 3 : 2)>(a, s, pdl);
+    case K_BWD_MID: return launch_one<N, K_BWD_MID, (MINB >= 3 ? 3 : 2)>(a, s, pdl);
+    case K_BWD_END: return launch_one<N, K_BWD_END, (MINB >= 3 ? 3 : 2)>(a, s, pdl);
     case K_EXIT_COMPLETE: return launch_one<N, K_EXIT_COMPLETE, MINB>(a, s, pdl);
     case K_RECON_FIRST: return launch_one<N, K_RECON_FIRST, MINB>(a, s, pdl);
     case K_RECON_MID: return launch_one<N, K_RECON_MID, MINB>(a, s, pdl);
