@@ -577,6 +577,13 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
       " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(z),
       "r"(smem_u32(bar)), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes, unsigned long long pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
                                           unsigned long long pol) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
@@ -741,6 +748,11 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
 #endif
   constexpr int BOX = tma_box(N), NBOX = N / BOX;
   constexpr bool NEED_V = kind_transmit(KIND) || kind_grad(KIND) || kind_recon(KIND);
+#ifdef PTYCHO_STASH_STG
+  constexpr bool STASH_BULK = false;
+#else
+  constexpr bool STASH_BULK = TMA && ENG::T * ENG::T == N;  // stash row written by one bulk copy
+#endif
   unsigned long long* mbar = (unsigned long long*)(smem + SM::bar);
   const int xal = LL.pos0 & ~3;                       // 16-B aligned start of the superset
   auto lidx_of = [&](int ln) { return ax == 0 ? wy0 + ln - a.ey0 : wx0 + ln - a.ex0; };
@@ -896,13 +908,29 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
           if (PL.transmit_cp) y.y = -y.y;
           const float2 phi = cmul(y, make_float2(cs, sn));
           xs[Q * k] = phi;
-          if (keep) st_stream(stp + Q * k, phi, pol);
+          if (!STASH_BULK && keep) st_stream(stp + Q * k, phi, pol);
         }
       };
       if (small_phases<P>(pv, a.sigma, [&](int k) { return q + Q * k; })) body(Bool<true>());
       else body(Bool<false>());
+      if constexpr (STASH_BULK) {
+        // the rolled buffer holds phi_s of this line in natural order = the stash row: one 8N-byte
+        // bulk copy (cp.async.bulk shared -> global) instead of N / Q stores per thread
+        if (keep) {
+          fence_proxy_async();
+          ENG::sync_line(bid);
+          if (q == 0) {
+            bulk_store(stp - q, ex, 8u * N, pol);
+            bulk_commit();
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < P; ++k) x[k] = xs[Q * k];
+      if constexpr (STASH_BULK) {
+        if (keep && q == 0) bulk_wait_read();  // the next exchange overwrites the buffer
+        ENG::sync_line(bid);
+      }
 #else
 #pragma unroll
       for (int k = 0; k < P; ++k) {
@@ -1135,6 +1163,9 @@ __device__ __forceinline__ void pass_body(const PassArgs& a, const int grp, int4
     }
   }
 
+  if constexpr (STASH_BULK && kind_transmit(KIND)) {
+    if (q == 0 && a.stash_store) bulk_wait();  // the stash row is in global memory before the CTA retires
+  }
   if (!PERSIST && a.advance) {
     __syncthreads();
     if (tid == 0) {
