@@ -273,15 +273,15 @@ ptycho_status ptycho_profile_chain(ptycho_ctx ctx, int32_t tile, int64_t first, 
 /* Measurement export (bench.py breakdown; SURVEY §8(d) "how it will be timed" item 5, mirroring
  * the paper's runtime breakdown): run ONE iteration exactly as ptycho_iterate (real work,
  * same results) but with the APPP slab pipelining off, so the phases are serial on this rank, and
- * return in ms_out[6], measured with CUDA events on the context stream:
+ * return in ms_out[8], measured with CUDA events on the context stream:
  *   [0] total, [1] compute (probe chains of all local tiles, all segments),
  *   [2] wait (P2P transport, receiving side: time in the READY waits, i.e. waiting for a peer to
  *       finish the region; 0 for the NCCL transport, whose receive time is in [3]),
  *   [3] comm (the rest of the APPP span: hop copies over NVLink / NCCL, local hops),
  *   [4] accumulated step (Alg. 1 steps 14-16),
  *   [5] sender hold (P2P, sending side: READY -> DONE spins = the peer's lateness + its copy of
- *       the region).  Collective (every rank must call it).
- * Synchronizes. */
+ *       the region), [6] receiving side: time of the copy kernels pulling peer AccBuf regions over
+ *       NVLink, [7] the bytes they pulled ([7] / [6] = the link rate).  Collective; synchronizes. */
 ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out);
 
 /* Ordering checks (compute-sanitizer is not available on this pool): a library

@@ -144,6 +144,8 @@ struct ptycho_ctx_s {
   unsigned long long p2p_timeout_ns = 600ull * 1000000000ull;
   std::vector<cudaEvent_t>* wait_ev = nullptr;    // ptycho_profile_iteration: events around P2P waits
   std::vector<cudaEvent_t>* signal_ev = nullptr;  // ... and around the senders' READY -> DONE spins
+  std::vector<cudaEvent_t>* copy_ev = nullptr;    // ... and around the receivers' NVLink pulls
+  double copy_bytes = 0.0;
 };
 
 static thread_local std::string g_create_err;
@@ -1434,13 +1436,23 @@ static ptycho_status hop_p2p(ptycho_ctx ctx, const Hop& h, size_t hid, bool send
   if (w1) CK(cudaEventRecord(w1, ctx->stream));
   ++ctx->launches;
   float* src_acc = (float*)(ctx->peer_ws[a.owner] + ctx->peer_acc[a.owner][a.k]);
+  cudaEvent_t c0 = nullptr, c1 = nullptr;
+  if (ctx->copy_ev) {  // ptycho_profile_iteration: the NVLink pull itself
+    CK(cudaEventCreate(&c0));
+    CK(cudaEventCreate(&c1));
+    ctx->copy_ev->push_back(c0);
+    ctx->copy_ev->push_back(c1);
+    CK(cudaEventRecord(c0, ctx->stream));
+  }
   for (int par = 0; par < 2; ++par) {
     SliceView vs = region_view(a, src_acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
     SliceView vd = region_view(b, b.acc, par, z0, z1, h.y0, h.y1, h.x0, h.x1);
     if (vs.nslices == 0) continue;
     CK(launch_copy2d(vd.base, vd.ld, vd.ss, vs.base, vs.ld, vs.ss, vs.rows, vs.cols, vs.nslices, h.add, ctx->stream));
     ++ctx->launches;
+    ctx->copy_bytes += 4.0 * vs.rows * vs.cols * vs.nslices;
   }
+  if (c1) CK(cudaEventRecord(c1, ctx->stream));
   CK(launch_p2p_post(peer_flag(a.owner, 1), ep, ctx->stream));
   ++ctx->launches;
   return PTYCHO_OK;
@@ -1654,19 +1666,21 @@ extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out
   if (!ms_out) return fail(ctx, PTYCHO_EARG, "ms_out is NULL");
   if (ctx->hve) return fail(ctx, PTYCHO_ESTATE, "profile_iteration: GD contexts only");
   CK(cudaSetDevice(ctx->device));
-  for (int i = 0; i < 6; ++i) ms_out[i] = 0.0;
+  for (int i = 0; i < 8; ++i) ms_out[i] = 0.0;
   size_t nmax = 0;
   for (const Tile& t : ctx->tiles) nmax = std::max(nmax, t.probes.size());
   if (nmax == 0) return PTYCHO_OK;
   const int64_t T = ctx->cfg.pass_period > 0 ? ctx->cfg.pass_period : (int64_t)nmax;
   const int64_t nseg = ((int64_t)nmax + T - 1) / T;
-  std::vector<cudaEvent_t> ev(4 * nseg + 1, nullptr), wait_ev, signal_ev;
+  std::vector<cudaEvent_t> ev(4 * nseg + 1, nullptr), wait_ev, signal_ev, copy_ev;
+  ctx->copy_bytes = 0.0;
   for (auto& e : ev) CK(cudaEventCreate(&e));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaEventRecord(ev[0], ctx->stream));
   ptycho_status st = PTYCHO_OK;
   ctx->wait_ev = &wait_ev;
   ctx->signal_ev = &signal_ev;
+  ctx->copy_ev = &copy_ev;
   for (int64_t j = 0; j < nseg && st == PTYCHO_OK; ++j) {
     if (j) CK(cudaEventRecord(ev[4 * j], ctx->stream));
     st = run_probes(ctx, j * T, T, CHAIN_GRAD);
@@ -1678,6 +1692,7 @@ extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out
   }
   ctx->wait_ev = nullptr;
   ctx->signal_ev = nullptr;
+  ctx->copy_ev = nullptr;
   if (st == PTYCHO_OK) {
     CK(cudaEventRecord(ev[4 * nseg], ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1703,10 +1718,16 @@ extern "C" ptycho_status ptycho_profile_iteration(ptycho_ctx ctx, double* ms_out
       ms_out[5] += ms;
     }
     ms_out[3] = std::max(0.0, appp - ms_out[2] - ms_out[5]);
+    for (size_t i = 0; i + 1 < copy_ev.size(); i += 2) {
+      CK(cudaEventElapsedTime(&ms, copy_ev[i], copy_ev[i + 1]));
+      ms_out[6] += ms;
+    }
+    ms_out[7] = ctx->copy_bytes;
   }
   for (auto e : ev) cudaEventDestroy(e);
   for (auto e : wait_ev) cudaEventDestroy(e);
   for (auto e : signal_ev) cudaEventDestroy(e);
+  for (auto e : copy_ev) cudaEventDestroy(e);
   return st == PTYCHO_OK ? PTYCHO_OK : (ctx->err.empty() ? fail(ctx, st, "profile_iteration failed") : st);
 }
 

@@ -346,10 +346,12 @@ class Ptycho:
 
     def profile_iteration(self):
         """One real iteration with serial phases; per-phase ms on this rank (collective)."""
-        ms = np.zeros(6, np.float64)
+        ms = np.zeros(8, np.float64)
         self._ck(lib.ptycho_profile_iteration(self.h, ms.ctypes.data))
-        return dict(zip(["total_ms", "compute_ms", "wait_ms", "comm_ms", "acc_step_ms", "sender_hold_ms"],
-                        (float(v) for v in ms)))
+        d = dict(zip(["total_ms", "compute_ms", "wait_ms", "comm_ms", "acc_step_ms", "sender_hold_ms",
+                      "nvlink_copy_ms", "nvlink_copy_bytes"], (float(v) for v in ms)))
+        d["nvlink_copy_gbs"] = d["nvlink_copy_bytes"] / (d["nvlink_copy_ms"] * 1e6) if d["nvlink_copy_ms"] > 0 else None
+        return d
 
     def debug_errors(self):
         """(error bits, checks_built) of the PTYCHO_DEBUG_CHECKS ordering checks (clears the bits)."""
