@@ -453,6 +453,16 @@ def main():
         allbd = [None] * world
         dist.all_gather_object(allbd, bd)
         breakdown = allbd
+    # NVLink roofline of the APPP exchange (north_star: "NVLink GB/s for the halo exchange"): the
+    # receivers' P2P copy kernels (bytes pulled from peer memory / their event time), against the
+    # 900 GB/s nominal per direction and the pool's measured 770 GB/s peer copy (B200_PROFILING.md)
+    rates = [r["nvlink_copy_gbs"] for r in breakdown if r.get("nvlink_copy_gbs")]
+    nvlink = None
+    if rates:
+        nvlink = {"achieved_gbs": min(rates), "achieved_gbs_per_rank": rates, "peak_gbs": 900.0,
+                  "peak_kind": "nominal per direction per GPU", "frac": min(rates) / 900.0,
+                  "measured_peer_copy_ref_gbs": 770.0, "frac_of_measured_ref": min(rates) / 770.0,
+                  "kernel": "copy2d_v4_kernel (receiver pulls the sender's AccBuf region in place)"}
 
     # ---- e2e: host measurements (pinned) -> device, one iteration, stitched V -> host, each step
     e2e = None
@@ -508,6 +518,7 @@ def main():
                 "gpu_launches": launches, "roofline": roofline, "clocks": clk.summary(),
                 "breakdown": {"note": "one extra iteration, APPP slab pipelining off (phases serial); ms per rank",
                               "ranks": breakdown},
+                "nvlink_roofline": nvlink,
                 "e2e": e2e, "cpu_baseline": cpu, "loss_after": loss, "appp": appp,
                 "paper_context": "GD small LT: 2310 probe-locations/s on 462 V100 (P:65-74)"}
         print(json.dumps(line), flush=True)
