@@ -418,7 +418,7 @@ extern "C" ptycho_status ptycho_set_tiles(ptycho_ctx ctx, int32_t rows, int32_t 
   // stay in the 126 MB L2 next to the streaming traffic, 8 do not -- LT-small on one B200 with
   // 8 virtual tiles: G = 3..5 452 probe-loc/s, G = 6 439, G = 8 439 (profiles/round1.md).
   int groups = std::min<int>((int)ctx->local.size(), 4);
-  if (const char* e = getenv("PTYCHO_TILE_STREAMS")) groups = std::max(1, std::min(groups, atoi(e)));
+  if (const char* e = getenv("PTYCHO_TILE_STREAMS")) groups = std::max(1, std::min((int)ctx->local.size(), atoi(e)));
   for (size_t i = 0; i < ctx->local.size(); ++i) {
     Tile& t = ctx->tiles[ctx->local[i]];
     if ((int)i < groups) {
