@@ -23,7 +23,7 @@ Parity status of each function (all pinned; see tests/test_oracle_pins.py):
   reconstruct .......... K=1 literal SGD, alpha=0 frozen equivalence (north_star invariant)
   stitch ............... round trip
   hve_decompose ........ SPEC worked example (3x3 mesh, 3x3 scan, one extra row -> centre tile holds all 9),
-                         1x1 trivial case, TileTooSmall predicate by brute force
+                         1x1 trivial case, TileTooSmall on a fine mesh
   hve_reconstruct ...... 1x1 == plain per-probe SGD, all-probes-everywhere == single tile, halos == owners'
                          interiors bitwise after every exchange
   seam_score ........... closed forms (constant field -> 0 jumps; a step placed on a tile border)
@@ -492,43 +492,37 @@ def accumulate_frozen(v0, probe, amps, centers, cfg, rows, cols, halo, tau=TAU):
 #   halos "augmented accordingly to cover all the additional circles", independent tile
 #   reconstructions, then "the voxels in each tile are pasted to the halos in neighboring GPUs",
 #   repeated until convergence; "two extra rows of probe locations for each tile".
-#   Readings (DESIGN.md §2 #33-#36): extra rows = a margin of (rows x scan step) pixels around the
-#   interior; the augmented rect is the bounding box of the interior and every assigned window,
-#   clipped to the object; one sweep of per-probe SGD per tile per iteration, then the copy-paste.
+#   Readings (DESIGN.md §2 #33-#35): extra rows = a margin of (rows x scan step) pixels around the
+#   interior for the probe assignment; the augmented halo is a width parameter like GD's (the paper:
+#   890 pm for HVE vs 600 pm for GD, "to cover all probe locations"), windows zero-extended past it
+#   (reading #12); one sweep of per-probe SGD per tile per iteration, then the copy-paste.
 # ---------------------------------------------------------------------------------
 class TileTooSmall(ValueError):
     """a tile's augmented halo reaches past its adjacent tiles' interiors (the paper's
     'NA' entries: each tile must be large enough to hold its neighbours' halos)."""
 
 
-def hve_decompose(height: int, width: int, rows: int, cols: int, centers, n: int, margin: int):
-    """Tiles with interior (uniform split, reading #14), probes = every probe whose centre lies in
-    the interior dilated by `margin` pixels (own + extra rows, ascending global index), and the
-    augmented rect = bounding box of the interior and those probes' N x N windows, clipped to the
-    object.  Raises TileTooSmall if an augmented rect extends past the interiors of the tile's
-    row/column neighbours (copy-paste could not fill that halo from an adjacent tile)."""
+def hve_decompose(height: int, width: int, rows: int, cols: int, centers, margin: int, halo: int):
+    """Tiles with interior (uniform split, reading #14), augmented rect = interior dilated by `halo`
+    and clipped (as tile_geometry), and probes = every probe whose centre lies in the interior
+    dilated by `margin` pixels (own + extra rows; ascending global index; a probe may sit on
+    several tiles).  Raises TileTooSmall if an augmented rect extends past the interiors of the
+    tile's row / column neighbours (copy-paste could not fill that halo from an adjacent tile)."""
     ys = split_extent(height, rows)
     xs = split_extent(width, cols)
-    tiles = []
-    for r in range(rows):
-        for c in range(cols):
-            y0, y1 = ys[r]
-            x0, x1 = xs[c]
-            probes = [i for i, (cy, cx) in enumerate(centers)
-                      if y0 - margin <= cy < y1 + margin and x0 - margin <= cx < x1 + margin]
-            ay0, ax0, ay1, ax1 = y0, x0, y1, x1
-            for i in probes:
-                cy, cx = int(centers[i][0]), int(centers[i][1])
-                ay0, ax0 = min(ay0, cy - n // 2), min(ax0, cx - n // 2)
-                ay1, ax1 = max(ay1, cy - n // 2 + n), max(ax1, cx - n // 2 + n)
-            aug = (max(0, ay0), max(0, ax0), min(height, ay1), min(width, ax1))
-            lo_y = ys[r - 1][0] if r > 0 else 0
-            hi_y = ys[r + 1][1] if r + 1 < rows else height
-            lo_x = xs[c - 1][0] if c > 0 else 0
-            hi_x = xs[c + 1][1] if c + 1 < cols else width
-            if aug[0] < lo_y or aug[2] > hi_y or aug[1] < lo_x or aug[3] > hi_x:
-                raise TileTooSmall(f"tile ({r},{c}): augmented rect {aug} reaches past its neighbours' interiors")
-            tiles.append(dict(r=r, c=c, interior=(y0, x0, y1, x1), ext=aug, probes=probes))
+    tiles = tile_geometry(height, width, rows, cols, halo)
+    for t in tiles:
+        r, c = t["r"], t["c"]
+        y0, x0, y1, x1 = t["interior"]
+        t["probes"] = [i for i, (cy, cx) in enumerate(centers)
+                       if y0 - margin <= cy < y1 + margin and x0 - margin <= cx < x1 + margin]
+        lo_y = ys[r - 1][0] if r > 0 else 0
+        hi_y = ys[r + 1][1] if r + 1 < rows else height
+        lo_x = xs[c - 1][0] if c > 0 else 0
+        hi_x = xs[c + 1][1] if c + 1 < cols else width
+        a = t["ext"]
+        if a[0] < lo_y or a[2] > hi_y or a[1] < lo_x or a[3] > hi_x:
+            raise TileTooSmall(f"tile ({r},{c}): augmented rect {a} reaches past its neighbours' interiors")
     return tiles
 
 
@@ -554,14 +548,14 @@ def hve_exchange(vks, tiles):
     return msgs
 
 
-def hve_reconstruct(v0, probe, amps, centers, cfg, rows, cols, margin, iterations, alpha, tau=TAU):
+def hve_reconstruct(v0, probe, amps, centers, cfg, rows, cols, margin, halo, iterations, alpha, tau=TAU):
     """HVE: per iteration, every tile independently runs one sweep of per-probe SGD
     (g = d f_i / d V, V[win ^ aug] -= alpha g, probes ascending) over its own + extra probes on its
     augmented tile, then the synchronous copy-paste exchange; finally stitch the interiors.
     Returns (V [S][H][W], [F per iteration: sum over every tile's probes, duplicates included], vks)."""
     n, sigma, c = cfg["n"], cfg["sigma"], cfg["prop_c"]
     slices, height, width = v0.shape
-    tiles = hve_decompose(height, width, rows, cols, centers, n, margin)
+    tiles = hve_decompose(height, width, rows, cols, centers, margin, halo)
     vks = decompose(v0, tiles)
     losses = []
     for _ in range(iterations):
