@@ -38,20 +38,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = True, defines=(), out=None) -> str:
-    """defines / out: experimental variants (e.g. ["PTYCHO_MIN2"], "lib/libptycho_a.so")."""
-    lib_out = out or LIB
-    if out is None and not force and not _stale():
-        return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+def _compile(defines, out, verbose):
+    """Start nvcc for every source of one library variant; returns (processes, objects, link cmd)."""
     inc, libdir = nccl_dirs()
     nvcc = os.environ.get("NVCC", "nvcc")
     common = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
     common += ["-D" + d for d in defines]
-    tag = "" if out is None else "_" + os.path.basename(out).replace(".so", "")
-    objs = []
-    procs = []
+    tag = "" if out == LIB else "_" + os.path.basename(out).replace(".so", "")
+    objs, procs = [], []
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src.replace(".cu", tag + ".o"))
         cmd = [nvcc] + common + ["-c", os.path.join(CSRC, src), "-o", obj]
@@ -59,18 +54,33 @@ def build(force: bool = False, verbose: bool = True, defines=(), out=None) -> st
             print(" ".join(cmd), flush=True)
         procs.append(subprocess.Popen(cmd))
         objs.append(obj)
-    for p in procs:
-        if p.wait() != 0:
-            raise RuntimeError("nvcc failed")
-    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib_out] + objs + ["-L", libdir, "-l:libnccl.so.2",
-                                                    "-Xlinker", "-rpath=" + libdir, "--cudart", "static"]
-    if verbose:
-        print(" ".join(link), flush=True)
-    subprocess.check_call(link)
+    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out] + objs + \
+        ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir, "--cudart", "static"]
+    return procs, link
+
+
+def build(force: bool = False, verbose: bool = True, defines=(), out=None) -> str:
+    """defines / out: experimental variants (e.g. ["PTYCHO_MIN2"], "lib/libptycho_a.so").  The
+    default build makes the product library and, compiled concurrently, the ordering-check variant
+    lib/libptycho_debug.so (-DPTYCHO_DEBUG_CHECKS; ptycho_debug_errors, tests/test_gpu_ordering.py)."""
+    lib_out = out or LIB
+    if out is None and not force and not _stale():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    variants = [(list(defines), lib_out)]
+    if out is None:
+        variants.append((list(defines) + ["PTYCHO_DEBUG_CHECKS"], DEBUG_LIB))
+    jobs = [_compile(d, o, verbose) for d, o in variants]
+    for procs, _ in jobs:
+        for p in procs:
+            if p.wait() != 0:
+                raise RuntimeError("nvcc failed")
+    for _, link in jobs:
+        if verbose:
+            print(" ".join(link), flush=True)
+        subprocess.check_call(link)
     if out is None:
         build_demo(verbose)
-        # ordering-check variant (ptycho_debug_errors; tests/test_gpu_ordering.py)
-        build(force=True, verbose=verbose, defines=list(defines) + ["PTYCHO_DEBUG_CHECKS"], out=DEBUG_LIB)
     return lib_out
 
 
