@@ -112,5 +112,8 @@ def seam(iters=20):
 
 if __name__ == "__main__":
     t0 = time.time()
-    {"perf": perf, "seam": seam}[sys.argv[1]]()
+    if sys.argv[1] == "seam" and len(sys.argv) > 2:
+        seam(int(sys.argv[2]))
+    else:
+        {"perf": perf, "seam": seam}[sys.argv[1]]()
     print(json.dumps({"elapsed_s": time.time() - t0}))
