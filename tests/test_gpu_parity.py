@@ -470,3 +470,52 @@ def test_appp_transport_api_states():
         p.set_appp_transport(PTYCHO_APPP_P2P)
     assert e.value.status == 3
     p.close()
+
+
+def test_stitch_pinned_zero_copy_equals_staged():
+    """ptycho_stitch into pinned host memory (gather kernels write through the mapped alias, one
+    launch per tile and slice parity, the bench's e2e path) == the staged per-slice copy into
+    pageable memory == the device output, bitwise."""
+    import torch
+    c = synth.CONFIGS["tiny"]
+    rng = np.random.default_rng(4)
+    v = rng.random((5, 150, 131), dtype=np.float32)
+    d = dict(n=64, slices=5, height=150, width=131, sigma=0.1, prop_c=3.135)
+    p = make(d, rows=2, cols=3)
+    p.set_scan(synth.scan_centers(150, 131, 3, 3))
+    p.allocate_workspace()
+    p.set_volume(v)
+    staged = p.stitch()
+    pinned = torch.empty((5, 150, 131), dtype=torch.float32).pin_memory()
+    p.stitch(pinned)
+    dev = torch.empty((5, 150, 131), dtype=torch.float32, device="cuda")
+    p.stitch(dev)
+    p.close()
+    assert np.array_equal(staged, v)
+    assert np.array_equal(pinned.numpy(), v)
+    assert np.array_equal(dev.cpu().numpy(), v)
+
+
+def test_profile_iteration_is_a_real_iteration():
+    """ptycho_profile_iteration runs one real iteration (phases serial): the result equals
+    ptycho_iterate's bitwise, and the phase times add up."""
+    d, probe, vt, centers, amps = _recon_problem()
+    v0 = (0.5 * vt).astype(np.float32)
+    outs = []
+    for prof in (False, True):
+        p = make(d, rows=2, cols=3, alpha=1.0, period=4)
+        p.set_scan(centers)
+        p.allocate_workspace()
+        p.set_probe(probe.astype(np.complex64))
+        p.load_measurements(amps[p.local_probes()])
+        p.set_volume(v0)
+        if prof:
+            bd = p.profile_iteration()
+            assert bd["compute_ms"] > 0 and bd["acc_step_ms"] > 0 and bd["comm_ms"] >= 0
+            assert bd["compute_ms"] + bd["comm_ms"] + bd["acc_step_ms"] <= bd["total_ms"] * 1.01
+            assert bd["wait_ms"] == 0 and bd["nvlink_copy_bytes"] == 0  # one rank: no peers
+        else:
+            p.iterate()
+        outs.append(p.stitch())
+        p.close()
+    assert np.array_equal(outs[0], outs[1])
