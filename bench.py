@@ -250,9 +250,9 @@ def main():
                     help="stash-free adjoint (PTYCHO_F_STASH_FREE): phi_s recomputed, 2-slice stash")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-async", choices=["auto", "on", "off"], default="auto",
-                    help="e2e: PTYCHO_AMP_ASYNC load overlapping the chains; auto = on at >= 4 ranks per "
-                         "host, where they share its upload bandwidth (N=4: e2e +16 %%), off "
-                         "below (N=1: -2.5 %%, N=2: -8 %%); profiles/round1.md")
+                    help="e2e: PTYCHO_AMP_ASYNC load overlapping the chains; auto = on (with the e2e "
+                         "warm-up, interleaved A/B: N=1 +1.2 %%, N=2 +1.2 %%, "
+                         "profiles/round2/e2e_async_ab_after_warmup.txt)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -467,11 +467,16 @@ def main():
     # ---- e2e: host measurements (pinned) -> device, one iteration, stitched V -> host, each step
     e2e = None
     if not args.no_e2e:
-        # the rationale is the host's shared upload bandwidth: ranks per HOST, not world size
-        e2e_async = args.e2e_async == "on" or (args.e2e_async == "auto" and env_int("LOCAL_WORLD_SIZE", world) >= 4)
+        e2e_async = args.e2e_async != "off"
         host_amp = torch.empty((nloc, n, n), dtype=torch.float32, pin_memory=True)
         p.read_measurements(0, nloc, host_amp)
         host_v = torch.empty((S, H, W), dtype=torch.float32, pin_memory=True) if rank == 0 else None
+        # untimed warm-up of the e2e calls: the first stitch over ranks opens NCCL's send/recv
+        # connections (0.6 s at N = 4, 0.9 s at N = 2: profiles/round2/e2e_parts.jsonl), a
+        # one-time cost that is not part of a step
+        p.load_measurements(host_amp, flags=PTYCHO_AMP_ASYNC if e2e_async else 0)
+        p.stitch(host_v, root=0, rank=rank)
+        p.synchronize()
         barrier()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)

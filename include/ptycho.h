@@ -69,10 +69,8 @@ typedef enum {
                                  /* overlaps the gradient passes.  The host buffer (pinned for real  */
                                  /* asynchrony) must stay valid and unchanged until                  */
                                  /* ptycho_synchronize.  Otherwise the flag is ignored (synchronous). */
-                                 /* Measured on B200, LT-small: with one rank per host the overlapped */
-                                 /* copy slows the chains by more than it saves (1 and 2 GPUs); with  */
-                                 /* 4 ranks sharing the host's upload bandwidth it wins (+16 % e2e),  */
-                                 /* so bench.py enables it at >= 4 ranks per host (LOCAL_WORLD_SIZE). */
+                                 /* Measured on B200, LT-small (e2e step = upload + iteration +     */
+                                 /* stitch): +1.2 % at 1 and at 2 GPUs against the synchronous load. */
 
 typedef struct {
   int32_t n;         /* N: probe window = detector side; 64, 256 or 1024                          */
