@@ -66,11 +66,13 @@ typedef enum {
                                  /* S even): return once the copies are enqueued.  They go straight */
                                  /* into the stores on a copy stream in chunks of 8 probes, and each */
                                  /* probe chain waits only for its own chunk, so the transfer        */
-                                 /* overlaps the gradient passes.  The host buffer (pinned for real  */
-                                 /* asynchrony) must stay valid and unchanged until                  */
-                                 /* ptycho_synchronize.  Otherwise the flag is ignored (synchronous). */
-                                 /* Measured on B200, LT-small (e2e step = upload + iteration +     */
-                                 /* stitch): +1.2 % at 1 and at 2 GPUs against the synchronous load. */
+                                 /* overlaps the gradient passes.  Pinned input with a device alias  */
+                                 /* (cudaHostAlloc, torch pin_memory) is read by 8-CTA upload kernels */
+                                 /* over PCIe; other host memory by copy-engine copies.  The host     */
+                                 /* buffer must stay valid and unchanged until ptycho_synchronize.   */
+                                 /* Otherwise the flag is ignored (synchronous).  Measured on B200,  */
+                                 /* LT-small: the 17.4 GB upload costs the iteration +50-80 ms (upload */
+                                 /* kernels) vs +265-300 ms (copy engine) vs +330 ms (synchronous).  */
 
 typedef struct {
   int32_t n;         /* N: probe window = detector side; 64, 256 or 1024                          */

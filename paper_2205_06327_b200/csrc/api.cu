@@ -729,6 +729,18 @@ static ptycho_status load_async(ptycho_ctx ctx, const float* amp, int64_t first_
   CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_copy, 0));
   int64_t chunk = 8;  // probes per event (32 MiB at N = 1024)
   if (const char* e = getenv("PTYCHO_AMP_CHUNK")) chunk = std::max(1, atoi(e));
+  // pinned host input with a device alias: upload kernels on the copy stream (events of a compute
+  // stream), else copy-engine copies (PTYCHO_AMP_CE=1 forces them)
+  const float* amp_dev = nullptr;
+  {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, amp) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer &&
+        ((uintptr_t)at.devicePointer & 15) == 0 && !getenv("PTYCHO_AMP_CE"))
+      amp_dev = (const float*)at.devicePointer;
+    cudaGetLastError();
+  }
+  int up_ctas = 8;
+  if (const char* e = getenv("PTYCHO_AMP_UPLOAD_CTAS")) up_ctas = std::max(1, atoi(e));
   struct Range {
     Tile* t;
     int64_t g, lo, hi;
@@ -760,8 +772,14 @@ static ptycho_status load_async(ptycho_ctx ctx, const float* amp, int64_t first_
       any = true;
       Tile& t = *r.t;
       const int64_t m = std::min(chunk, r.hi - p);
-      CK(cudaMemcpyAsync(t.amp + (size_t)(p - r.g) * n2, amp + (size_t)(p - first_local) * n2,
-                         (size_t)m * n2 * sizeof(float), cudaMemcpyHostToDevice, ctx->copy_stream));
+      if (amp_dev) {
+        CK(launch_upload(t.amp + (size_t)(p - r.g) * n2, amp_dev + (size_t)(p - first_local) * n2,
+                         (long long)m * (long long)n2, up_ctas, ctx->copy_stream));
+        ++ctx->launches;
+      } else {
+        CK(cudaMemcpyAsync(t.amp + (size_t)(p - r.g) * n2, amp + (size_t)(p - first_local) * n2,
+                           (size_t)m * n2 * sizeof(float), cudaMemcpyHostToDevice, ctx->copy_stream));
+      }
       if (ne == t.amp_pool.size()) {
         t.amp_pool.push_back(nullptr);
         CK(cudaEventCreateWithFlags(&t.amp_pool.back(), cudaEventDisableTiming));

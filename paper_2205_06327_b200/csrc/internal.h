@@ -114,6 +114,8 @@ cudaError_t launch_set_batch(int4* desc, const int2* centers, const int* list, i
 // *desc = probe v of the tile (v clamped to [0, nk))
 cudaError_t launch_set_desc(int4* desc, const int2* centers, int v, int nk, int n, cudaStream_t stream);
 cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t stream);
+// dst[0, n) = src[0, n): src the device alias of pinned host memory, both 16-B aligned, n % 4 == 0
+cudaError_t launch_upload(float* dst, const float* src, long long n, int ctas, cudaStream_t stream);
 cudaError_t launch_sum_double(const double* parts, int n, double* out, cudaStream_t stream);
 // APPP peer-to-peer transport: flag kernels (one thread each; see kernels.cu)
 // timeout_ns = 0: wait without limit; otherwise a timed-out wait sets *err (host-mapped) and returns

@@ -1777,6 +1777,30 @@ cudaError_t launch_fill(float* p, long long n, float v, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Host -> device upload through the device alias of pinned host memory (PCIe reads by a few
+// CTAs, 64 B per thread in flight): the asynchronous measurement load uses it instead of copy-engine
+// copies, whose completion events the chains' cross-stream waits observe late (DESIGN.md §8 e2e).
+__global__ void __launch_bounds__(1024) upload_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
+                                                      long long n4) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    const float4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n4; i += stride) dst[i] = src[i];
+}
+
+cudaError_t launch_upload(float* dst, const float* src, long long n, int ctas, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  upload_kernel<<<ctas, 1024, 0, stream>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst),
+                                           n / 4);
+  return cudaGetLastError();
+}
+
 // deterministic fixed-order sum of the per-CTA loss partials
 __global__ void sum_double_kernel(const double* parts, int n, double* out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
